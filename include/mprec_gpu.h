@@ -1,0 +1,202 @@
+/*
+ * mprec_gpu.h -- C ABI of the B200-native GMRES / CPR / CPTR3 solve path.
+ *
+ * Drop-in boundary for the reference `mprec` hot path.  Each
+ * entry point names the reference interface it replaces.  Plain pointers and
+ * sizes only; no C++ or torch types cross this boundary.  All `const double*`
+ * / `double*` vector arguments are HOST pointers unless the name ends in
+ * `_dev`.  Every function returns an mprec_status; on failure
+ * mprec_gpu_last_error() / mprec_gpu_error_payload() give the message and the
+ * cell/row payload (thread-local), mirroring the exception classes of
+ * proj/include/mprec/errors.hpp:9-59.
+ *
+ * Threading: a handle's setup is not thread-safe; apply/solve calls on one
+ * handle are serialised on the handle's CUDA stream; distinct handles are
+ * independent (one handle per system, any number per process/GPU).
+ */
+#ifndef MPREC_GPU_H
+#define MPREC_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: proj/include/mprec/errors.hpp:9-59 */
+typedef enum mprec_status {
+    MPREC_OK = 0,
+    MPREC_DIMENSION = 1,      /* DimensionError                                   */
+    MPREC_INDEX = 2,          /* IndexError                                       */
+    MPREC_SINGULAR_BLOCK = 3, /* SingularBlockError{cell_id} (payload = cell / i) */
+    MPREC_ZERO_PIVOT = 4,     /* ZeroPivotError{row_id}      (payload = row)      */
+    MPREC_SETUP = 5,          /* SetupError                                       */
+    MPREC_CONFIG = 6,         /* ConfigError                                      */
+    MPREC_INTERNAL = 7,
+    MPREC_CUDA = 8,           /* CUDA runtime failure (no GPU, OOM, ...)           */
+} mprec_status;
+
+/* MethodSpec (proj/include/mprec/scaling.hpp:10-20); parse_method strings
+ * "ilu0", "cpr-amg", "cptr3-amg" (scaling.cpp:5-15). */
+typedef enum mprec_method {
+    MPREC_METHOD_ILU0 = 0,
+    MPREC_METHOD_CPR_AMG = 1,
+    MPREC_METHOD_CPTR3_AMG = 3,
+} mprec_method;
+
+/* AMGParams (proj/include/mprec/amg.hpp:12-16). */
+typedef struct mprec_amg_params {
+    double strength_threshold; /* 0.25 */
+    int max_coarse_size;       /* 1000 */
+    int max_levels;            /* 25   */
+} mprec_amg_params;
+
+/* Uniform-layout BlockMatrix (proj/include/mprec/block_matrix.hpp:50-101):
+ * n_cells block rows, nb unknowns per cell in (s..., P, T) order
+ * (field_layout.hpp:62-66), block columns sorted ascending per row with the
+ * diagonal block present (BlockMatrix::assemble, block_matrix.cpp:32-69),
+ * values = nnzb column-major nb x nb blocks (Eigen's default storage).  The
+ * caller keeps ownership; create copies to the device. */
+typedef struct mprec_bsr {
+    int n_cells;
+    int nb;
+    const int* row_ptr; /* n_cells + 1 */
+    const int* col_idx; /* row_ptr[n_cells] */
+    const double* values;
+} mprec_bsr;
+
+/* Scalar CSR (ScalarMatrix, scalar_matrix.hpp:20-62), canonical form. */
+typedef struct mprec_csr {
+    int n_rows;
+    const int* row_ptr;
+    const int* col_idx;
+    const double* values;
+} mprec_csr;
+
+/* SolveResult (gmres.hpp:28-36) + SolveOutcome (harness.hpp:79-83). */
+typedef struct mprec_solve_result {
+    int iterations;             /* of the last attempt */
+    int converged;
+    int breakdown;
+    int attempts;               /* tolerance-tightening attempts (harness.cpp:209) */
+    int history_len;            /* entries written to `history` */
+    double final_true_residual; /* ||b - A x|| / ||b|| on the ORIGINAL system */
+    double setup_s;             /* left_scale + build_preconditioner */
+    double solve_s;             /* all GMRES attempts */
+} mprec_solve_result;
+
+typedef struct mprec_gpu_system mprec_gpu_system; /* opaque */
+typedef struct mprec_gpu_amg mprec_gpu_amg;       /* opaque */
+typedef struct mprec_gpu_ilu mprec_gpu_ilu;       /* opaque */
+
+const char* mprec_gpu_last_error(void);
+int mprec_gpu_error_payload(void);
+/* sm / device sanity: returns MPREC_OK if a CUDA device is usable. */
+int mprec_gpu_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* mem_bytes);
+
+/* ---- whole-system path --------------------------------------------------- */
+
+/* Copies A to the device.  Replaces constructing the BlockMatrix the solve
+ * path starts from (block_matrix.cpp:32-69); non-uniform layouts are not
+ * representable here (MPREC_DIMENSION). */
+int mprec_gpu_create(const mprec_bsr* a, mprec_gpu_system** out);
+
+/* left_scale (scaling.cpp:149-158) + build_preconditioner (stages.cpp:129-138)
+ * with ScalingOptions{Block, second_scaling_from_original=false}.  amg may be
+ * NULL (defaults).  b: host rhs (n_cells*nb). */
+int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg,
+                    const double* b);
+
+/* StagePreconditioner::apply (stages.cpp:36-59) / apply_stage (stages.hpp:54). */
+int mprec_gpu_apply(mprec_gpu_system* h, const double* r, double* z);
+int mprec_gpu_apply_stage(mprec_gpu_system* h, int stage, const double* r, double* z);
+
+/* y = A x (which=0: original A, BlockMatrix::apply block_matrix.cpp:103-114;
+ * which=1: scaled Ā, the GMRES operator ScalarMatrix::apply on a_flat_). */
+int mprec_gpu_spmv(mprec_gpu_system* h, int which, const double* x, double* y);
+
+/* solve_system after setup (harness.cpp:198-218): GMRES on (Ā, b̄) with the
+ * stage preconditioner, true residual on the original A, <=3 attempts with
+ * tol <- tol*0.5*tol/true_resid.  x: host out (n).  history (optional, may be
+ * NULL): relative preconditioned residuals of the last attempt. */
+int mprec_gpu_solve(mprec_gpu_system* h, double tol, int max_iter, double* x,
+                    mprec_solve_result* out, double* history, int history_cap);
+
+/* Same as mprec_gpu_solve but leaves x on the device (x_dev may be NULL: the
+ * handle keeps it); used to time the device-resident hot path. */
+int mprec_gpu_solve_dev(mprec_gpu_system* h, double tol, int max_iter, double* x_dev,
+                        mprec_solve_result* out);
+
+/* Whole solve_system (harness.cpp:190-219) from host buffers: create + setup
+ * + solve + destroy. */
+int mprec_gpu_solve_system(const mprec_bsr* a, const double* b, int method, double tol,
+                           int max_iter, double* x, mprec_solve_result* out);
+
+/* Parity diagnostics. */
+int mprec_gpu_get_scaled(mprec_gpu_system* h, double* abar_values, double* b_bar);
+int mprec_gpu_get_ilu(mprec_gpu_system* h, double* lu_values);
+int mprec_gpu_n_stages(mprec_gpu_system* h, int* n_stages);
+/* stage: index of an AMG stage (CPR: 0; CPTR3: 0 = C_TT, 1 = B_PP). */
+int mprec_gpu_stage_amg(mprec_gpu_system* h, int stage, mprec_gpu_amg** amg);
+
+/* Release (also releases the AMG handles returned by mprec_gpu_stage_amg). */
+void mprec_gpu_destroy(mprec_gpu_system* h);
+
+/* ---- sub-solver entry points (amg.hpp:21-56, ilu0.hpp:9-24) -------------- */
+
+/* AMGHierarchy::setup (amg.cpp:188-214) on a scalar CSR. */
+int mprec_gpu_amg_create(const mprec_csr* a, const mprec_amg_params* p, mprec_gpu_amg** out);
+/* AMGHierarchy::apply (amg.cpp:233-238): one V(1,1) cycle, zero initial guess. */
+int mprec_gpu_amg_apply(mprec_gpu_amg* h, const double* r, double* x);
+int mprec_gpu_amg_n_levels(mprec_gpu_amg* h, int* n_levels);
+/* level sizes; nnz_p = 0 on level 0 (levels_[0].p unused, amg.hpp:47) */
+int mprec_gpu_amg_level_info(mprec_gpu_amg* h, int level, int* n, int* nnz_a, int* nnz_p);
+/* which: 0 = A_l, 1 = P_l (n_{l-1} x n_l), 2 = R_l = P_l^T */
+int mprec_gpu_amg_get_csr(mprec_gpu_amg* h, int level, int which, int* row_ptr, int* col_idx,
+                          double* values);
+/* C/F splitting of level l (1 = C) that produced level l+1 (rs_coarsen). */
+int mprec_gpu_amg_get_cf(mprec_gpu_amg* h, int level, signed char* cf);
+void mprec_gpu_amg_destroy(mprec_gpu_amg* h);
+
+/* ILU0Factor::factor / apply (ilu0.cpp:7-59) on a BSR (nb = 1: scalar ILU(0)). */
+int mprec_gpu_ilu_create(const mprec_bsr* a, mprec_gpu_ilu** out);
+int mprec_gpu_ilu_apply(mprec_gpu_ilu* h, const double* r, double* y);
+int mprec_gpu_ilu_get(mprec_gpu_ilu* h, double* lu_values);
+void mprec_gpu_ilu_destroy(mprec_gpu_ilu* h);
+
+/* gmres (gmres.cpp:8-106) with A = BSR operator (flat order) and
+ * preconditioner: prec_kind 0 = identity, 1 = AMG handle, 2 = ILU handle. */
+int mprec_gpu_gmres(const mprec_bsr* a, const double* b, int prec_kind, void* prec,
+                    double tol, int max_iter, double* x, mprec_solve_result* out,
+                    double* history, int history_cap);
+
+/* ---- measurement ---------------------------------------------------------- */
+
+/* Kernel classes timed with CUDA events on the handle's stream when profiling
+ * is on (mprec_gpu_profile). */
+typedef enum mprec_kernel_class {
+    MPREC_K_SPMV = 0,      /* BSR SpMV (GMRES operator, true residual)        */
+    MPREC_K_SPMV_COL = 1,  /* scoped residual update z = r - Ā[:,f] x_f       */
+    MPREC_K_ILU_FWD = 2,
+    MPREC_K_ILU_BWD = 3,
+    MPREC_K_GS = 4,        /* symmetric Gauss-Seidel sweeps (all levels)      */
+    MPREC_K_CSR = 5,       /* level residual / restriction / prolongation     */
+    MPREC_K_COARSE = 6,    /* coarsest dense solve                            */
+    MPREC_K_MGS = 7,       /* Arnoldi MGS dot/axpy                            */
+    MPREC_K_BLAS1 = 8,     /* scale/copy/norm/gather/scatter                  */
+    MPREC_K_COUNT = 9
+} mprec_kernel_class;
+
+int mprec_gpu_profile(mprec_gpu_system* h, int enable);
+/* accumulated since the last reset: total device ms, launches, algorithmic bytes */
+int mprec_gpu_kernel_stats(mprec_gpu_system* h, int kclass, double* ms, int64_t* launches,
+                           double* bytes);
+int mprec_gpu_reset_stats(mprec_gpu_system* h);
+/* number of kernel launches issued on the handle since the last reset */
+int mprec_gpu_launch_count(mprec_gpu_system* h, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPREC_GPU_H */

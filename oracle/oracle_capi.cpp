@@ -1,0 +1,355 @@
+// oracle_capi.cpp -- C entry points of the CPU oracle (TEST INFRASTRUCTURE).
+// Same signatures as include/mprec_gpu.h with the prefix `orc_`, so the parity
+// tests drive both sides through one wrapper (tests/_native.py).
+#include <chrono>
+#include <cstring>
+#include <string>
+
+#include "../include/mprec_gpu.h"
+#include "oracle.hpp"
+
+using namespace oracle;
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_payload = -1;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return MPREC_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        g_payload = e.payload;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        g_payload = -1;
+        return MPREC_INTERNAL;
+    }
+}
+
+AMGParams to_params(const mprec_amg_params* p) {
+    AMGParams q;
+    if (p) {
+        q.strength_threshold = p->strength_threshold;
+        q.max_coarse_size = p->max_coarse_size;
+        q.max_levels = p->max_levels;
+    }
+    return q;
+}
+
+Csr to_csr(const mprec_csr* a) {
+    Csr m;
+    m.rows = m.cols = a->n_rows;
+    m.rp.assign(a->row_ptr, a->row_ptr + a->n_rows + 1);
+    const int nnz = a->row_ptr[a->n_rows];
+    m.ci.assign(a->col_idx, a->col_idx + nnz);
+    m.v.assign(a->values, a->values + nnz);
+    return m;
+}
+
+Bsr to_bsr(const mprec_bsr* a) { return Bsr::create(a->n_cells, a->nb, a->row_ptr, a->col_idx, a->values); }
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+struct orc_system {
+    Bsr a;
+    Vec b;
+    ScaledSystem sc;
+    StagePreconditioner prec;
+    bool ready = false;
+    double setup_s = 0.0;
+};
+struct orc_amg {
+    AMGHierarchy h;
+};
+struct orc_ilu {
+    Ilu0Block f;
+};
+
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+int orc_error_payload(void) { return g_payload; }
+
+int orc_create(const mprec_bsr* a, orc_system** out) {
+    return guard([&] {
+        auto* h = new orc_system;
+        try {
+            h->a = to_bsr(a);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int orc_setup(orc_system* h, int method, const mprec_amg_params* amg, const double* b) {
+    return guard([&] {
+        if (method != MPREC_METHOD_ILU0 && method != MPREC_METHOD_CPR_AMG && method != MPREC_METHOD_CPTR3_AMG)
+            throw Error(CONFIG, "unknown method id " + std::to_string(method));
+        h->ready = false;
+        h->b.assign(b, b + h->a.dim());
+        const double t0 = now_s();
+        h->sc = left_scale(h->a, h->b, Method(method));
+        h->prec = build_preconditioner(h->sc, to_params(amg));
+        h->setup_s = now_s() - t0;
+        h->ready = true;
+    });
+}
+
+int orc_apply(orc_system* h, const double* r, double* z) {
+    return guard([&] {
+        if (!h->ready) throw Error(SETUP, "setup not done");
+        const Vec y = h->prec.apply(Vec(r, r + h->a.dim()));
+        std::memcpy(z, y.data(), y.size() * sizeof(double));
+    });
+}
+
+int orc_apply_stage(orc_system* h, int stage, const double* r, double* z) {
+    return guard([&] {
+        if (!h->ready) throw Error(SETUP, "setup not done");
+        if (stage < 0 || stage >= int(h->prec.stages.size())) throw Error(INDEX, "stage out of range");
+        const Vec y = h->prec.apply_stage(stage, Vec(r, r + h->a.dim()));
+        std::memcpy(z, y.data(), y.size() * sizeof(double));
+    });
+}
+
+int orc_spmv(orc_system* h, int which, const double* x, double* y) {
+    return guard([&] {
+        const Vec xv(x, x + h->a.dim());
+        Vec r;
+        if (which == 0)
+            r = h->a.apply_block(xv);
+        else {
+            if (!h->ready) throw Error(SETUP, "setup not done");
+            r = h->sc.a_bar.apply_flat(xv);
+        }
+        std::memcpy(y, r.data(), r.size() * sizeof(double));
+    });
+}
+
+int orc_solve(orc_system* h, double tol, int max_iter, double* x, mprec_solve_result* out, double* history,
+              int history_cap) {
+    return guard([&] {
+        if (!h->ready) throw Error(SETUP, "setup not done");
+        const double t0 = now_s();
+        GmresOptions opts;
+        opts.tol = tol;
+        opts.max_iter = max_iter;
+        const Op orig = [h](const Vec& v) { return h->a.apply_block(v); };
+        const Op abar = [h](const Vec& v) { return h->sc.a_bar.apply_flat(v); };
+        const Op mop = [h](const Vec& v) { return h->prec.apply(v); };
+        SolveResult res;
+        int attempts = 0;
+        for (int attempt = 0; attempt < 3; ++attempt) {
+            ++attempts;
+            res = gmres(h->a.dim(), abar, h->sc.b_bar, mop, opts);
+            res.final_true_residual = residual_check(orig, h->b, res.x);
+            if (!res.converged || res.final_true_residual <= tol) break;
+            opts.tol *= 0.5 * tol / res.final_true_residual;
+        }
+        if (res.converged && res.final_true_residual > tol) res.converged = false;
+        std::memcpy(x, res.x.data(), res.x.size() * sizeof(double));
+        out->iterations = res.iterations;
+        out->converged = res.converged;
+        out->breakdown = res.breakdown;
+        out->attempts = attempts;
+        out->final_true_residual = res.final_true_residual;
+        out->setup_s = h->setup_s;
+        out->solve_s = now_s() - t0;
+        int nh = int(res.residual_history.size());
+        if (history && history_cap < nh) nh = history_cap;
+        if (history)
+            for (int i = 0; i < nh; ++i) history[i] = res.residual_history[i];
+        out->history_len = history ? nh : int(res.residual_history.size());
+    });
+}
+
+int orc_get_scaled(orc_system* h, double* abar, double* bbar) {
+    return guard([&] {
+        if (!h->ready) throw Error(SETUP, "setup not done");
+        if (abar) std::memcpy(abar, h->sc.a_bar.val.data(), h->sc.a_bar.val.size() * sizeof(double));
+        if (bbar) std::memcpy(bbar, h->sc.b_bar.data(), h->sc.b_bar.size() * sizeof(double));
+    });
+}
+
+int orc_get_ilu(orc_system* h, double* lu) {
+    return guard([&] {
+        if (!h->ready) throw Error(SETUP, "setup not done");
+        std::memcpy(lu, h->prec.ilu.lu.val.data(), h->prec.ilu.lu.val.size() * sizeof(double));
+    });
+}
+
+int orc_n_stages(orc_system* h, int* n) {
+    return guard([&] { *n = h->ready ? int(h->prec.stages.size()) : 0; });
+}
+
+int orc_stage_amg(orc_system* h, int stage, orc_amg** amg) {
+    return guard([&] {
+        if (!h->ready) throw Error(SETUP, "setup not done");
+        if (stage < 0 || stage >= int(h->prec.stages.size()) || h->prec.stages[stage].kind != Stage::AMG)
+            throw Error(INDEX, "not an AMG stage");
+        // non-owning view: the oracle AMG object lives in the preconditioner
+        *amg = reinterpret_cast<orc_amg*>(h->prec.stages[stage].amg.get());
+    });
+}
+
+void orc_destroy(orc_system* h) { delete h; }
+
+// ---- sub-solvers ----------------------------------------------------------
+
+int orc_amg_create(const mprec_csr* a, const mprec_amg_params* p, orc_amg** out) {
+    return guard([&] {
+        auto* h = new AMGHierarchy(AMGHierarchy::setup(to_csr(a), to_params(p)));
+        *out = reinterpret_cast<orc_amg*>(h);
+    });
+}
+
+int orc_amg_apply(orc_amg* hh, const double* r, double* x) {
+    return guard([&] {
+        auto* h = reinterpret_cast<AMGHierarchy*>(hh);
+        const int n = h->levels.front().a.rows;
+        const Vec y = h->apply(Vec(r, r + n));
+        std::memcpy(x, y.data(), y.size() * sizeof(double));
+    });
+}
+
+int orc_amg_n_levels(orc_amg* hh, int* n) {
+    return guard([&] { *n = reinterpret_cast<AMGHierarchy*>(hh)->n_levels(); });
+}
+
+int orc_amg_level_info(orc_amg* hh, int level, int* n, int* nnz_a, int* nnz_p) {
+    return guard([&] {
+        auto* h = reinterpret_cast<AMGHierarchy*>(hh);
+        if (level < 0 || level >= h->n_levels()) throw Error(INDEX, "level out of range");
+        const auto& L = h->levels[level];
+        *n = L.a.rows;
+        *nnz_a = L.a.nnz();
+        *nnz_p = level == 0 ? 0 : L.p.nnz();
+    });
+}
+
+int orc_amg_get_csr(orc_amg* hh, int level, int which, int* rp, int* ci, double* v) {
+    return guard([&] {
+        auto* h = reinterpret_cast<AMGHierarchy*>(hh);
+        if (level < 0 || level >= h->n_levels()) throw Error(INDEX, "level out of range");
+        const auto& L = h->levels[level];
+        const Csr& m = which == 0 ? L.a : (which == 1 ? L.p : L.r);
+        if (rp) std::memcpy(rp, m.rp.data(), m.rp.size() * sizeof(int));
+        if (ci) std::memcpy(ci, m.ci.data(), m.ci.size() * sizeof(int));
+        if (v) std::memcpy(v, m.v.data(), m.v.size() * sizeof(double));
+    });
+}
+
+int orc_amg_get_cf(orc_amg* hh, int level, signed char* cf) {
+    return guard([&] {
+        auto* h = reinterpret_cast<AMGHierarchy*>(hh);
+        if (level < 0 || level + 1 >= h->n_levels()) throw Error(INDEX, "level has no coarsening");
+        const auto& m = h->levels[level].cf;
+        for (size_t i = 0; i < m.size(); ++i) cf[i] = m[i];
+    });
+}
+
+void orc_amg_destroy(orc_amg* hh) { delete reinterpret_cast<AMGHierarchy*>(hh); }
+
+int orc_ilu_create(const mprec_bsr* a, orc_ilu** out) {
+    return guard([&] {
+        auto* h = new orc_ilu;
+        try {
+            h->f = Ilu0Block::factor(to_bsr(a));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int orc_ilu_apply(orc_ilu* h, const double* r, double* y) {
+    return guard([&] {
+        const Vec o = h->f.apply(Vec(r, r + h->f.lu.dim()));
+        std::memcpy(y, o.data(), o.size() * sizeof(double));
+    });
+}
+
+int orc_ilu_get(orc_ilu* h, double* lu) {
+    return guard([&] { std::memcpy(lu, h->f.lu.val.data(), h->f.lu.val.size() * sizeof(double)); });
+}
+
+void orc_ilu_destroy(orc_ilu* h) { delete h; }
+
+int orc_gmres(const mprec_bsr* a, const double* b, int prec_kind, void* prec, double tol, int max_iter,
+              double* x, mprec_solve_result* out, double* history, int history_cap) {
+    return guard([&] {
+        const Bsr m = to_bsr(a);
+        const int n = m.dim();
+        const Op aop = [&m](const Vec& v) { return m.apply_flat(v); };
+        Op mop;
+        if (prec_kind == 0)
+            mop = [](const Vec& v) { return v; };
+        else if (prec_kind == 1)
+            mop = [prec](const Vec& v) { return reinterpret_cast<AMGHierarchy*>(prec)->apply(v); };
+        else if (prec_kind == 2)
+            mop = [prec](const Vec& v) { return reinterpret_cast<orc_ilu*>(prec)->f.apply(v); };
+        else
+            throw Error(CONFIG, "unknown preconditioner kind");
+        GmresOptions o;
+        o.tol = tol;
+        o.max_iter = max_iter;
+        const double t0 = now_s();
+        const SolveResult res = gmres(n, aop, Vec(b, b + n), mop, o);
+        std::memcpy(x, res.x.data(), res.x.size() * sizeof(double));
+        out->iterations = res.iterations;
+        out->converged = res.converged;
+        out->breakdown = res.breakdown;
+        out->attempts = 1;
+        out->final_true_residual = res.final_true_residual;
+        out->setup_s = 0.0;
+        out->solve_s = now_s() - t0;
+        int nh = int(res.residual_history.size());
+        if (history && history_cap < nh) nh = history_cap;
+        if (history)
+            for (int i = 0; i < nh; ++i) history[i] = res.residual_history[i];
+        out->history_len = history ? nh : int(res.residual_history.size());
+    });
+}
+
+// Reference-literal scalar route for validating the block restatement:
+// flatten (block_matrix.cpp:116-128) + ILU0Factor on the scalar CSR.
+int orc_ilu_scalar_factor(const mprec_bsr* a, double* lu_flat_values) {
+    return guard([&] {
+        const Bsr m = to_bsr(a);
+        const Ilu0Scalar f = Ilu0Scalar::factor(m.to_scalar());
+        std::memcpy(lu_flat_values, f.lu.v.data(), f.lu.v.size() * sizeof(double));
+    });
+}
+int orc_ilu_scalar_apply(const mprec_bsr* a, const double* r, double* y) {
+    return guard([&] {
+        const Bsr m = to_bsr(a);
+        const Ilu0Scalar f = Ilu0Scalar::factor(m.to_scalar());
+        const Vec o = f.apply(Vec(r, r + m.dim()));
+        std::memcpy(y, o.data(), o.size() * sizeof(double));
+    });
+}
+int orc_spmv_scalar(const mprec_bsr* a, const double* x, double* y) {
+    return guard([&] {
+        const Bsr m = to_bsr(a);
+        const Vec o = m.to_scalar().apply(Vec(x, x + m.dim()));
+        std::memcpy(y, o.data(), o.size() * sizeof(double));
+    });
+}
+int orc_level_sets(const mprec_csr* a, int* levels) {
+    return guard([&] {
+        const auto l = level_sets_lower(to_csr(a));
+        std::memcpy(levels, l.data(), l.size() * sizeof(int));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// amg_cycle.cu -- the V(1,1)-cycle (AMGHierarchy::cycle/apply, amg.cpp:216-238):
+// K14 symmetric Gauss-Seidel sweeps, K15 residual / restriction / prolongation
+// (CSR SpMV), K13 coarsest solve as a dense GEMV with the precomputed inverse.
+//
+// Gauss-Seidel keeps the reference's natural-order semantics
+// (sym_gauss_seidel, amg.cpp:25-43): the forward sweep uses updated x_k for
+// k < i and previous x_k for k > i, the backward sweep the mirror image.  It is
+// dependency-scheduled, not replaced: one warp per row, rows claimed in sweep
+// order from an atomic counter, the new iterate is written to a fresh buffer
+// pre-filled with the kPending sentinel and consumers poll the producer's value
+// (double buffering also makes the "old" reads race-free for any pattern).
+#include "mprec.cuh"
+
+namespace mg {
+namespace {
+
+__device__ __forceinline__ double ld_poll(const double* p) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    } while (v == kPending);
+    return __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ void st_pub(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
+}
+
+constexpr int kGsWarps = 8;
+
+template <int DIR>
+__global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp, const int* __restrict__ ci,
+                                                      const double* __restrict__ v, const int* __restrict__ diag,
+                                                      const double* __restrict__ b, const double* __restrict__ xold,
+                                                      double* xnew, int n, int* counter) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(counter, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= n) return;
+        const int i = DIR > 0 ? t : n - 1 - t;
+        double acc = 0.0;
+        for (int k = rp[i] + lane; k < rp[i + 1]; k += 32) {
+            const int j = __ldg(ci + k);
+            if (j == i) continue;
+            const double a = __ldg(v + k);
+            double xj;
+            if (DIR > 0 ? (j < i) : (j > i))
+                xj = ld_poll(xnew + j);
+            else
+                xj = xold ? __ldg(xold + j) : 0.0;
+            acc += a * xj;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) st_pub(xnew + i, (b[i] - acc) / v[diag[i]]);
+    }
+}
+
+// 8 lanes per row; mode 0: y = Ax, 1: y = b - Ax, 2: y = y + Ax
+__global__ void __launch_bounds__(256) k_csr(const int* __restrict__ rp, const int* __restrict__ ci,
+                                             const double* __restrict__ v, const double* __restrict__ x, double* y,
+                                             const double* __restrict__ b, int n, int mode) {
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    const int row = int(g >> 3), s = int(g & 7);
+    double acc = 0.0;
+    if (row < n)
+        for (int k = rp[row] + s; k < rp[row + 1]; k += 8) acc += __ldg(v + k) * __ldg(x + __ldg(ci + k));
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if (row < n && s == 0) y[row] = mode == 0 ? acc : (mode == 1 ? b[row] - acc : y[row] + acc);
+}
+
+// y = M x, M row-major n x n, warp per row
+__global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ m, int n, const double* __restrict__ x,
+                                              double* y) {
+    const int lane = threadIdx.x & 31;
+    const int row = int((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (row >= n) return;
+    const double* mr = m + (int64_t)row * n;
+    double acc = 0.0;
+    for (int j = lane; j < n; j += 32) acc += mr[j] * x[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[row] = acc;
+}
+
+}  // namespace
+
+void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, double* xnew, int dir, bool xold_zero) {
+    const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 4.0 * a.n + 24.0 * a.n;
+    Ctx::Scope sc(&c, MPREC_K_GS, bytes);
+    int* ctr = c.counters.p + 4;
+    MG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), c.s));
+    const int blocks = std::max(1, std::min((a.n + kGsWarps - 1) / kGsWarps, c.sm_count * 8));
+    if (dir > 0)
+        k_gs<1><<<blocks, kGsWarps * 32, 0, c.s>>>(a.rp, a.ci, a.v, a.diag, b, xold_zero ? nullptr : xold, xnew, a.n,
+                                                   ctr);
+    else
+        k_gs<-1><<<blocks, kGsWarps * 32, 0, c.s>>>(a.rp, a.ci, a.v, a.diag, b, xold_zero ? nullptr : xold, xnew,
+                                                    a.n, ctr);
+    check_launch("gs_sweep");
+}
+
+void csr_spmv(Ctx& c, const CsrView& a, const double* x, double* y, const double* b, bool add_to_y, int kclass) {
+    if (a.n == 0) return;
+    const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 8.0 * a.m + 8.0 * a.n + ((b || add_to_y) ? 8.0 * a.n : 0.0);
+    Ctx::Scope sc(&c, kclass, bytes);
+    const int mode = add_to_y ? 2 : (b ? 1 : 0);
+    const int64_t threads = (int64_t)a.n * 8;
+    k_csr<<<int((threads + 255) / 256), 256, 0, c.s>>>(a.rp, a.ci, a.v, x, y, b, a.n, mode);
+    check_launch("csr_spmv");
+}
+
+void dense_gemv(Ctx& c, const double* m, int n, const double* x, double* y) {
+    if (n == 0) return;
+    Ctx::Scope sc(&c, MPREC_K_COARSE, 8.0 * n * n + 16.0 * n);
+    const int64_t threads = (int64_t)n * 32;
+    k_gemv<<<int((threads + 255) / 256), 256, 0, c.s>>>(m, n, x, y);
+    check_launch("dense_gemv");
+}
+
+// amg.cpp:216-231
+void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
+    AmgLevel& L = *lv[l];
+    if (l == n_levels() - 1) {
+        dense_gemv(c, coarse_inv.p, nco, r, x);
+        return;
+    }
+    AmgLevel& N = *lv[l + 1];
+    const int64_t n = L.n;
+    // x = 0; sym GS
+    fill_pending(c, L.xf.p, n);
+    gs_sweep(c, L.a, r, nullptr, L.xf.p, +1, true);
+    fill_pending(c, x, n);
+    gs_sweep(c, L.a, r, L.xf.p, x, -1, false);
+    // rc = R (r - A x)
+    csr_spmv(c, L.a, x, L.t.p, r, false, MPREC_K_CSR);
+    csr_spmv(c, N.r.view(), L.t.p, N.b.p, nullptr, false, MPREC_K_CSR);
+    cycle(c, l + 1, N.b.p, N.x.p);
+    // x += P ec
+    csr_spmv(c, N.p.view(), N.x.p, x, nullptr, true, MPREC_K_CSR);
+    // post sym GS
+    fill_pending(c, L.xf.p, n);
+    gs_sweep(c, L.a, r, x, L.xf.p, +1, false);
+    fill_pending(c, x, n);
+    gs_sweep(c, L.a, r, L.xf.p, x, -1, false);
+}
+
+// amg.cpp:233-238
+void Amg::apply(Ctx& c, const double* r, double* x) { cycle(c, 0, r, x); }
+
+}  // namespace mg

@@ -1,0 +1,893 @@
+// amg_setup_exact.cu -- AMG setup on the device: K7 strength, K8/K9 exact
+// Ruge-Stueben C/F splitting, K10 direct interpolation, K11 transpose, K12
+// Galerkin SpGEMM, K13 coarsest dense LU + inverse.  Restates
+// rs_coarsen / AMGHierarchy::setup (proj/src/amg.cpp:47-214) with results
+// bitwise equal to the oracle (file compiled with -fmad=false):
+//
+//  * strength (amg.cpp:53-68): m_i = max(0, max_{k!=i} -a_ik); j strong iff
+//    -a_ij >= theta*m_i; S in CSR order, S^T in ascending row order.
+//  * first pass (amg.cpp:70-111): the lazy max-heap on (lambda, -i) with
+//    lambda only ever incremented selects, at every step, the undecided node
+//    of maximal lambda and lowest index.  It is emulated EXACTLY by one warp
+//    over per-lambda hierarchical bitmaps (bucket queue): find the highest
+//    non-empty bucket, find-first-set through three bitmap levels, then apply
+//    the selection's F-marks and lambda increments with warp-parallel
+//    neighbourhood updates (removals and insertions in separate phases so the
+//    summary bits stay consistent).  Parallel coarsenings (PMIS/HMIS/CLJP)
+//    would change the splitting and are not used.
+//  * second/third passes (amg.cpp:113-143) are ascending-i sequential with
+//    F->C promotions only.  Promotions can only add C points, so a node that
+//    needs no promotion under the current marks never will: a parallel filter
+//    finds the candidates, and one warp replays exactly the reference loop on
+//    the (few) candidates in ascending order.
+//  * interpolation (amg.cpp:145-185) thread per row, same summation order,
+//    entries pushed only if w != 0.
+//  * Galerkin R(AP) (scalar_matrix.cpp:120-151): per output entry the products
+//    are summed from 0.0 in ascending A-column order, symbolic zeros kept.
+#include <cub/cub.cuh>
+
+#include "mprec.cuh"
+
+namespace mg {
+namespace {
+
+enum : signed char { kU = 0, kC = 1, kF = 2 };
+
+// ---------------------------------------------------------------- strength --
+__global__ void k_strength_count(const int* rp, const int* ci, const double* v, int n, double theta, double* mrow,
+                                 int* scnt, int* stcnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double m = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+        if (ci[k] != i) {
+            const double t = -v[k];
+            m = (m < t) ? t : m;  // std::max(m, t)
+        }
+    mrow[i] = m;
+    int cnt = 0;
+    if (m > 0.0) {
+        const double thr = theta * m;
+        for (int k = rp[i]; k < rp[i + 1]; ++k) {
+            const int j = ci[k];
+            if (j != i && -v[k] >= thr) {
+                ++cnt;
+                atomicAdd(stcnt + j, 1);
+            }
+        }
+    }
+    scnt[i] = cnt;
+}
+
+__global__ void k_strength_fill(const int* rp, const int* ci, const double* v, int n, double theta, const double* mrow,
+                                const int* srp, int* sci, const int* strp, int* stfill, int* stci) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double m = mrow[i];
+    if (!(m > 0.0)) return;
+    const double thr = theta * m;
+    int o = srp[i];
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        if (j != i && -v[k] >= thr) {
+            sci[o++] = j;
+            const int pos = atomicAdd(stfill + j, 1);
+            stci[strp[j] + pos] = i;
+        }
+    }
+}
+
+// insertion sort of each CSR row by column (carrying optional values)
+__global__ void k_sort_rows(const int* rp, int* ci, double* v, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int a = rp[i], b = rp[i + 1];
+    for (int p = a + 1; p < b; ++p) {
+        const int key = ci[p];
+        const double kv = v ? v[p] : 0.0;
+        int q = p - 1;
+        while (q >= a && ci[q] > key) {
+            ci[q + 1] = ci[q];
+            if (v) v[q + 1] = v[q];
+            --q;
+        }
+        ci[q + 1] = key;
+        if (v) v[q + 1] = kv;
+    }
+}
+
+// ------------------------------------------------------- RS first pass ------
+struct Buckets {
+    unsigned long long *l0, *l1, *l2;
+    int n0, n1, n2;
+    int* cnt;
+};
+
+__device__ __forceinline__ void bq_remove(const Buckets& q, int i, int b) {
+    const int w0 = i >> 6;
+    const unsigned long long bit = 1ull << (i & 63);
+    const unsigned long long o0 = atomicAnd(q.l0 + (int64_t)b * q.n0 + w0, ~bit);
+    if ((o0 & ~bit) == 0ull) {
+        const int w1 = w0 >> 6;
+        const unsigned long long bit1 = 1ull << (w0 & 63);
+        const unsigned long long o1 = atomicAnd(q.l1 + (int64_t)b * q.n1 + w1, ~bit1);
+        if ((o1 & ~bit1) == 0ull) atomicAnd(q.l2 + (int64_t)b * q.n2 + (w1 >> 6), ~(1ull << (w1 & 63)));
+    }
+    atomicSub(q.cnt + b, 1);
+}
+
+__device__ __forceinline__ void bq_insert(const Buckets& q, int i, int b) {
+    const int w0 = i >> 6;
+    const unsigned long long bit = 1ull << (i & 63);
+    const unsigned long long o0 = atomicOr(q.l0 + (int64_t)b * q.n0 + w0, bit);
+    if (o0 == 0ull) {
+        const int w1 = w0 >> 6;
+        const unsigned long long o1 = atomicOr(q.l1 + (int64_t)b * q.n1 + w1, 1ull << (w0 & 63));
+        if (o1 == 0ull) atomicOr(q.l2 + (int64_t)b * q.n2 + (w1 >> 6), 1ull << (w1 & 63));
+    }
+    atomicAdd(q.cnt + b, 1);
+}
+
+__global__ void k_rs_init(const int* scnt, const int* stcnt, int n, signed char* mark, int* lam, Buckets q, int* lmax) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int l = stcnt[i];
+    lam[i] = l;
+    if (scnt[i] == 0 && l == 0) {
+        mark[i] = kF;  // unconnected: smoothing handles it alone
+        return;
+    }
+    mark[i] = kU;
+    const int w0 = i >> 6;
+    atomicOr(q.l0 + (int64_t)l * q.n0 + w0, 1ull << (i & 63));
+    atomicAdd(q.cnt + l, 1);
+}
+
+__global__ void k_bq_summary(const unsigned long long* lo, unsigned long long* hi, int nlo, int nhi, int nbuckets) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nhi * nbuckets) return;
+    const int b = int(t / nhi), w = int(t - (int64_t)b * nhi);
+    unsigned long long acc = 0;
+    for (int s = 0; s < 64; ++s) {
+        const int idx = w * 64 + s;
+        if (idx < nlo && lo[(int64_t)b * nlo + idx] != 0ull) acc |= 1ull << s;
+    }
+    hi[(int64_t)b * nhi + w] = acc;
+}
+
+__global__ void k_max_int(const int* a, int n, int* out) {
+    int m = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) m = max(m, a[i]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// One warp: exact emulation of the lazy-heap greedy (amg.cpp:86-111).
+__global__ void __launch_bounds__(32) k_rs_select(const int* srp, const int* sci, const int* strp, const int* stci,
+                                                  signed char* mark, int* lam, Buckets q, int nbuckets, int* inc,
+                                                  int* jlist, int* klist) {
+    const int lane = threadIdx.x;
+    __shared__ int nj_sh, nk_sh;
+    int hi = nbuckets - 1;
+    for (;;) {
+        // highest non-empty bucket
+        for (;;) {
+            const int b = hi - lane;
+            const bool ne = b >= 0 && ((volatile int*)q.cnt)[b] > 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, ne);
+            if (bal) {
+                hi -= __ffs(bal) - 1;
+                break;
+            }
+            hi -= 32;
+            if (hi < 0) break;
+        }
+        if (hi < 0) return;
+        // lowest index in bucket hi: first non-zero top-level word
+        int first = 0x7fffffff;
+        for (int w = lane; w < q.n2; w += 32)
+            if (((volatile unsigned long long*)q.l2)[(int64_t)hi * q.n2 + w] != 0ull) {
+                first = w;
+                break;
+            }
+        for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+        int i = 0;
+        if (lane == 0) {
+            const unsigned long long x2 = ((volatile unsigned long long*)q.l2)[(int64_t)hi * q.n2 + first];
+            const int w1 = first * 64 + __ffsll((long long)x2) - 1;
+            const unsigned long long x1 = ((volatile unsigned long long*)q.l1)[(int64_t)hi * q.n1 + w1];
+            const int w0 = w1 * 64 + __ffsll((long long)x1) - 1;
+            const unsigned long long x0 = ((volatile unsigned long long*)q.l0)[(int64_t)hi * q.n0 + w0];
+            i = w0 * 64 + __ffsll((long long)x0) - 1;
+            mark[i] = kC;
+            bq_remove(q, i, hi);
+            nj_sh = 0;
+            nk_sh = 0;
+        }
+        i = __shfl_sync(0xffffffffu, i, 0);
+        __syncwarp();
+        // phase d: undecided j in S^T_i become F
+        for (int jj = strp[i] + lane; jj < strp[i + 1]; jj += 32) {
+            const int j = stci[jj];
+            if (((volatile signed char*)mark)[j] == kU) {
+                mark[j] = kF;
+                bq_remove(q, j, lam[j]);
+                jlist[atomicAdd(&nj_sh, 1)] = j;
+            }
+        }
+        __syncwarp();
+        const int nj = ((volatile int*)&nj_sh)[0];
+        // phase e1: count the increments of every undecided k in S_j
+        for (int t = 0; t < nj; ++t) {
+            const int j = jlist[t];
+            for (int kk = srp[j] + lane; kk < srp[j + 1]; kk += 32) {
+                const int k = sci[kk];
+                if (((volatile signed char*)mark)[k] == kU) {
+                    if (atomicAdd(inc + k, 1) == 0) klist[atomicAdd(&nk_sh, 1)] = k;
+                }
+            }
+        }
+        __syncwarp();
+        const int nk = ((volatile int*)&nk_sh)[0];
+        // phase e2a: removals
+        for (int t = lane; t < nk; t += 32) {
+            const int k = klist[t];
+            bq_remove(q, k, lam[k]);
+        }
+        __syncwarp();
+        // phase e2b: insertions at the incremented lambda
+        int mx = -1;
+        for (int t = lane; t < nk; t += 32) {
+            const int k = klist[t];
+            const int nl = lam[k] + ((volatile int*)inc)[k];
+            inc[k] = 0;
+            lam[k] = nl;
+            bq_insert(q, k, nl);
+            mx = max(mx, nl);
+        }
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        hi = max(hi, mx);
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------- RS second and third passes --
+__device__ __forceinline__ bool in_row(const int* sci, int a, int b, int key) {
+    while (a < b) {
+        const int m = (a + b) >> 1;
+        const int v = sci[m];
+        if (v == key) return true;
+        if (v < key)
+            a = m + 1;
+        else
+            b = m;
+    }
+    return false;
+}
+
+// candidates of the second pass: F with S_i != {} that would promote now
+__global__ void k_rs2_cand(const int* srp, const int* sci, const signed char* mark, int n, int* flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int need = 0;
+    if (mark[i] == kF && srp[i + 1] > srp[i]) {
+        const int a = srp[i], b = srp[i + 1];
+        for (int p = a; p < b && !need; ++p) {
+            const int j = sci[p];
+            if (mark[j] != kF) continue;
+            bool shared = false;
+            for (int kk = srp[j]; kk < srp[j + 1]; ++kk) {
+                const int k = sci[kk];
+                if (mark[k] == kC && in_row(sci, a, b, k)) {
+                    shared = true;
+                    break;
+                }
+            }
+            if (!shared) need = 1;
+        }
+    }
+    flag[i] = need;
+}
+
+// S_i is sorted ascending (CSR order of a canonical matrix), so `in_row` works.
+__global__ void __launch_bounds__(32) k_rs2_seq(const int* srp, const int* sci, signed char* mark, const int* cand,
+                                                int ncand) {
+    const int lane = threadIdx.x;
+    __shared__ int cil[4096];
+    __shared__ int ncil;
+    for (int t = 0; t < ncand; ++t) {
+        const int i = cand[t];
+        if (((volatile signed char*)mark)[i] != kF) continue;
+        const int a = srp[i], b = srp[i + 1];
+        if (lane == 0) ncil = 0;
+        __syncwarp();
+        for (int p = a + lane; p < b; p += 32) {
+            const int j = sci[p];
+            if (((volatile signed char*)mark)[j] == kC) {
+                const int pos = atomicAdd(&ncil, 1);
+                if (pos < 4096) cil[pos] = j;
+            }
+        }
+        __syncwarp();
+        for (int p = a; p < b; ++p) {
+            const int j = sci[p];
+            if (((volatile signed char*)mark)[j] != kF) continue;
+            const int nci = min(((volatile int*)&ncil)[0], 4096);
+            bool shared = false;
+            const int ja = srp[j], jb = srp[j + 1];
+            for (int kk = ja + lane; kk < jb && !shared; kk += 32) {
+                const int k = sci[kk];
+                for (int e = 0; e < nci; ++e)
+                    if (((volatile int*)cil)[e] == k) {
+                        shared = true;
+                        break;
+                    }
+            }
+            shared = __any_sync(0xffffffffu, shared);
+            if (!shared && lane == 0) {
+                mark[j] = kC;
+                const int pos = ncil;
+                if (pos < 4096) cil[pos] = j;
+                ncil = pos + 1;
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_rs3_cand(const int* srp, const int* sci, const signed char* mark, int n, int* flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int need = 0;
+    if (mark[i] == kF && srp[i + 1] > srp[i]) {
+        need = 1;
+        for (int p = srp[i]; p < srp[i + 1]; ++p)
+            if (mark[sci[p]] == kC) {
+                need = 0;
+                break;
+            }
+    }
+    flag[i] = need;
+}
+
+__global__ void __launch_bounds__(32) k_rs3_seq(const int* srp, const int* sci, signed char* mark, const int* cand,
+                                                int ncand) {
+    const int lane = threadIdx.x;
+    for (int t = 0; t < ncand; ++t) {
+        const int i = cand[t];
+        bool has_c = false;
+        for (int p = srp[i] + lane; p < srp[i + 1]; p += 32)
+            if (((volatile signed char*)mark)[sci[p]] == kC) has_c = true;
+        has_c = __any_sync(0xffffffffu, has_c);
+        if (!has_c && lane == 0) mark[i] = kC;
+        __syncwarp();
+    }
+}
+
+__global__ void k_compact(const int* flag, const int* pos, int n, int* list) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) list[pos[i]] = i;
+}
+
+__global__ void k_is_c(const signed char* mark, int n, int* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = mark[i] == kC ? 1 : 0;
+}
+
+// ---------------------------------------------------------- interpolation --
+// mode 0: count entries per row; mode 1: fill (prp = row pointer)
+__global__ void k_interp(const int* rp, const int* ci, const double* v, int n, double theta, const double* mrow,
+                         const int* scnt, const signed char* mark, const int* cpos, int mode, int* pcnt,
+                         const int* prp, int* pci, double* pv) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // coarse_id[j] = cpos[j] when mark[j] == C
+    if (mark[i] == kC) {
+        if (mode == 0)
+            pcnt[i] = 1;
+        else {
+            pci[prp[i]] = cpos[i];
+            pv[prp[i]] = 1.0;
+        }
+        return;
+    }
+    if (scnt[i] == 0) {
+        if (mode == 0) pcnt[i] = 0;
+        return;
+    }
+    const double thr = theta * mrow[i];
+    double sum_neg_all = 0.0, sum_pos_all = 0.0, sum_neg_c = 0.0, sum_pos_c = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        if (j == i) continue;
+        const double a = v[k];
+        if (a < 0.0)
+            sum_neg_all += a;
+        else
+            sum_pos_all += a;
+        if (mark[j] == kC && -a >= thr) {
+            if (a < 0.0)
+                sum_neg_c += a;
+            else
+                sum_pos_c += a;
+        }
+    }
+    double aii = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+        if (ci[k] == i) aii = v[k];
+    if (sum_pos_c == 0.0) aii += sum_pos_all;
+    const double alpha = sum_neg_c != 0.0 ? sum_neg_all / sum_neg_c : 0.0;
+    const double beta = sum_pos_c != 0.0 ? sum_pos_all / sum_pos_c : 0.0;
+    int cnt = 0, o = mode ? prp[i] : 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        if (j == i || !(-v[k] >= thr) || mark[j] != kC) continue;  // j in S_i and coarse
+        const double aij = v[k];
+        const double w = aij < 0.0 ? -alpha * aij / aii : -beta * aij / aii;
+        if (w != 0.0) {
+            if (mode) {
+                pci[o] = cpos[j];
+                pv[o] = w;
+                ++o;
+            }
+            ++cnt;
+        }
+    }
+    if (mode == 0) pcnt[i] = cnt;
+}
+
+// -------------------------------------------------------------- transpose --
+__global__ void k_col_count(const int* ci, int nnz, int* cnt) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < nnz) atomicAdd(cnt + ci[k], 1);
+}
+
+__global__ void k_transpose_fill(const int* rp, const int* ci, const double* v, int n, const int* trp, int* fillc,
+                                 int* tci, double* tv) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int c = ci[k];
+        const int pos = trp[c] + atomicAdd(fillc + c, 1);
+        tci[pos] = i;
+        tv[pos] = v[k];
+    }
+}
+
+// ----------------------------------------------------------------- SpGEMM --
+__global__ void k_prod_count(const int* arp, const int* aci, const int* brp, int n, int* m) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int s = 0;
+    for (int k = arp[i]; k < arp[i + 1]; ++k) s += brp[aci[k] + 1] - brp[aci[k]];
+    m[i] = s;
+}
+
+// Warp per output row.  mode 0: unique-column count; mode 1: fill.
+__global__ void __launch_bounds__(256) k_spgemm(const int* arp, const int* aci, const double* av, const int* brp,
+                                                const int* bci, const double* bv, int n, int cap, int* scol,
+                                                double* sval, int* sfirst, int mode, int* cnt, const int* crp,
+                                                int* cci, double* cv) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int* col = scol + wid * cap;
+    double* val = sval + wid * cap;
+    int* first = sfirst + wid * cap;
+    for (int64_t row = wid; row < n; row += nw) {
+        const int i = int(row);
+        int m = 0;
+        for (int ka = arp[i]; ka < arp[i + 1]; ++ka) {
+            const int j = aci[ka];
+            const double a = av[ka];
+            const int b0 = brp[j], len = brp[j + 1] - b0;
+            for (int t = lane; t < len; t += 32) {
+                col[m + t] = bci[b0 + t];
+                val[m + t] = a * bv[b0 + t];
+            }
+            m += len;
+        }
+        __syncwarp();
+        int u = 0;
+        for (int p = lane; p < m; p += 32) {
+            const int cp = col[p];
+            int f = 1;
+            for (int q = 0; q < p; ++q)
+                if (col[q] == cp) {
+                    f = 0;
+                    break;
+                }
+            first[p] = f;
+            u += f;
+        }
+        for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+        __syncwarp();
+        if (mode == 0) {
+            if (lane == 0) cnt[i] = u;
+        } else {
+            const int base = crp[i];
+            for (int p = lane; p < m; p += 32) {
+                if (!first[p]) continue;
+                const int cp = col[p];
+                int rank = 0;
+                double s = 0.0;
+                for (int q = 0; q < m; ++q) {
+                    const int cq = col[q];
+                    if (first[q] && cq < cp) ++rank;
+                    if (cq == cp) s += val[q];
+                }
+                cci[base + rank] = cp;
+                cv[base + rank] = s;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_diag_pos(const int* rp, const int* ci, int n, int* diag, int* missing) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int d = -1;
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+        if (ci[k] == i) d = k;
+    diag[i] = d;
+    if (d < 0) atomicOr(missing, 1);
+}
+
+// ------------------------------------------------------------- dense LU -----
+__global__ void k_csr_to_dense(const int* rp, const int* ci, const double* v, int n, double* d) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) d[(int64_t)ci[k] * n + i] = v[k];
+}
+
+// Single CTA: Eigen::PartialPivLU unblocked path, column-major.
+__global__ void __launch_bounds__(1024) k_dense_lu(double* a, int n, int* perm, double* scale_out) {
+    __shared__ double sv[1024];
+    __shared__ int si[1024];
+    __shared__ double sbest;
+    __shared__ int sp;
+    const int t = threadIdx.x;
+    // scale = max |a|
+    double mx = 0.0;
+    for (int64_t e = t; e < (int64_t)n * n; e += 1024) mx = fmax(mx, fabs(a[e]));
+    sv[t] = mx;
+    __syncthreads();
+    for (int s = 512; s > 0; s >>= 1) {
+        if (t < s) sv[t] = fmax(sv[t], sv[t + s]);
+        __syncthreads();
+    }
+    if (t == 0) *scale_out = sv[0];
+    for (int i = t; i < n; i += 1024) perm[i] = i;
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        // first max |a(i,k)|, i >= k
+        double best = -1.0;
+        int bi = 0x7fffffff;
+        for (int i = k + t; i < n; i += 1024) {
+            const double x = fabs(a[(int64_t)k * n + i]);
+            if (x > best) {
+                best = x;
+                bi = i;
+            }
+        }
+        sv[t] = best;
+        si[t] = bi;
+        __syncthreads();
+        for (int s = 512; s > 0; s >>= 1) {
+            if (t < s) {
+                const double o = sv[t + s];
+                const int oi = si[t + s];
+                if (o > sv[t] || (o == sv[t] && oi < si[t])) {
+                    sv[t] = o;
+                    si[t] = oi;
+                }
+            }
+            __syncthreads();
+        }
+        if (t == 0) {
+            sbest = sv[0];
+            sp = si[0];
+        }
+        __syncthreads();
+        const double bst = sbest;
+        const int p = sp;
+        if (bst != 0.0) {
+            if (p != k) {
+                for (int j = t; j < n; j += 1024) {
+                    const double x = a[(int64_t)j * n + k];
+                    a[(int64_t)j * n + k] = a[(int64_t)j * n + p];
+                    a[(int64_t)j * n + p] = x;
+                }
+                if (t == 0) {
+                    const int x = perm[k];
+                    perm[k] = perm[p];
+                    perm[p] = x;
+                }
+            }
+            __syncthreads();
+            const double d = a[(int64_t)k * n + k];
+            for (int i = k + 1 + t; i < n; i += 1024) a[(int64_t)k * n + i] = a[(int64_t)k * n + i] / d;
+        }
+        __syncthreads();
+        const int rem = n - k - 1;
+        for (int64_t e = t; e < (int64_t)rem * rem; e += 1024) {
+            const int jj = k + 1 + int(e / rem), ii = k + 1 + int(e % rem);
+            a[(int64_t)jj * n + ii] = a[(int64_t)jj * n + ii] - a[(int64_t)k * n + ii] * a[(int64_t)jj * n + k];
+        }
+        __syncthreads();
+    }
+}
+
+// thread per column j of the inverse: oracle DenseLU::solve_inplace(e_j);
+// out row-major (out[i*n + j] = inv(i,j)), which is also the coalesced layout.
+__global__ void k_dense_inv(const double* lu, const int* perm, int n, double* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    for (int i = 0; i < n; ++i) out[(int64_t)i * n + j] = (perm[i] == j) ? 1.0 : 0.0;
+    for (int jj = 0; jj < n; ++jj) {
+        const double xj = out[(int64_t)jj * n + j];
+        for (int i = jj + 1; i < n; ++i)
+            out[(int64_t)i * n + j] = out[(int64_t)i * n + j] - lu[(int64_t)jj * n + i] * xj;
+    }
+    for (int jj = n - 1; jj >= 0; --jj) {
+        const double xj = out[(int64_t)jj * n + j] / lu[(int64_t)jj * n + jj];
+        out[(int64_t)jj * n + j] = xj;
+        for (int i = 0; i < jj; ++i) out[(int64_t)i * n + j] = out[(int64_t)i * n + j] - lu[(int64_t)jj * n + i] * xj;
+    }
+}
+
+}  // namespace
+
+// =========================================================== host helpers ==
+struct Scratch {
+    DBuf<char> tmp;
+};
+
+// out[0] = 0, out[i+1] = sum_{k<=i} in[k]; returns out[n]
+static int scan(Ctx& c, Scratch& s, const int* in, int* out, int n) {
+    MG_CUDA(cudaMemsetAsync(out, 0, sizeof(int), c.s));
+    if (n == 0) return 0;
+    size_t bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out + 1, n, c.s);
+    s.tmp.ensure(bytes + 16);
+    cub::DeviceScan::InclusiveSum(s.tmp.p, bytes, in, out + 1, n, c.s);
+    check_launch("scan");
+    int total = 0;
+    MG_CUDA(cudaMemcpyAsync(&total, out + n, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    return total;
+}
+
+static inline int nblk(int64_t n, int t = 256) { return int(std::max<int64_t>(1, (n + t - 1) / t)); }
+
+// C = A * B (scalar_matrix.cpp:120-151), exact
+static void spgemm(Ctx& c, Scratch& s, const CsrView& a, const CsrView& b, DCsr& out) {
+    const int n = a.n;
+    DBuf<int> m(n > 0 ? n : 1), cnt(n > 0 ? n : 1);
+    out.n = n;
+    out.m = b.m;
+    out.rp.alloc(n + 1);
+    if (n == 0) {
+        MG_CUDA(cudaMemsetAsync(out.rp.p, 0, sizeof(int), c.s));
+        out.nnz = 0;
+        return;
+    }
+    k_prod_count<<<nblk(n), 256, 0, c.s>>>(a.rp, a.ci, b.rp, n, m.p);
+    int cap = 0;
+    {
+        DBuf<int> mx(1);
+        MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), c.s));
+        k_max_int<<<std::min(nblk(n), 1024), 256, 0, c.s>>>(m.p, n, mx.p);
+        MG_CUDA(cudaMemcpyAsync(&cap, mx.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+    }
+    cap = std::max(cap, 1);
+    // per-warp scratch of `cap` products; keep the total under ~512 MB
+    const int64_t budget = int64_t(512) << 20;
+    const int64_t wcap = std::max<int64_t>(8, budget / (int64_t(cap) * 16));
+    const int warps = int(std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(n, int64_t(c.sm_count) * 16), wcap)));
+    const int blocks = (warps + 7) / 8;
+    const int64_t nw = int64_t(blocks) * 8;
+    DBuf<int> scol(nw * cap), sfirst(nw * cap);
+    DBuf<double> sval(nw * cap);
+    k_spgemm<<<blocks, 256, 0, c.s>>>(a.rp, a.ci, a.v, b.rp, b.ci, b.v, n, cap, scol.p, sval.p, sfirst.p, 0, cnt.p,
+                                      nullptr, nullptr, nullptr);
+    check_launch("spgemm count");
+    out.nnz = scan(c, s, cnt.p, out.rp.p, n);
+    out.ci.alloc(std::max(out.nnz, 1));
+    out.v.alloc(std::max(out.nnz, 1));
+    k_spgemm<<<blocks, 256, 0, c.s>>>(a.rp, a.ci, a.v, b.rp, b.ci, b.v, n, cap, scol.p, sval.p, sfirst.p, 1, nullptr,
+                                      out.rp.p, out.ci.p, out.v.p);
+    check_launch("spgemm fill");
+    c.sync();
+}
+
+// R = P^T (scalar_matrix.cpp:98-105)
+static void transpose(Ctx& c, Scratch& s, const DCsr& p, DCsr& r) {
+    r.n = p.m;
+    r.m = p.n;
+    r.nnz = p.nnz;
+    DBuf<int> cnt(std::max(r.n, 1)), fillc(std::max(r.n, 1));
+    MG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * r.n, c.s));
+    MG_CUDA(cudaMemsetAsync(fillc.p, 0, sizeof(int) * r.n, c.s));
+    if (p.nnz) k_col_count<<<nblk(p.nnz), 256, 0, c.s>>>(p.ci.p, p.nnz, cnt.p);
+    r.rp.alloc(r.n + 1);
+    scan(c, s, cnt.p, r.rp.p, r.n);
+    r.ci.alloc(std::max(r.nnz, 1));
+    r.v.alloc(std::max(r.nnz, 1));
+    k_transpose_fill<<<nblk(p.n), 256, 0, c.s>>>(p.rp.p, p.ci.p, p.v.p, p.n, r.rp.p, fillc.p, r.ci.p, r.v.p);
+    k_sort_rows<<<nblk(r.n), 256, 0, c.s>>>(r.rp.p, r.ci.p, r.v.p, r.n);
+    check_launch("transpose");
+}
+
+static void diag_positions(Ctx& c, const CsrView& a, DBuf<int>& diag) {
+    diag.alloc(std::max(a.n, 1));
+    int* missing = c.counters.p + 8;
+    MG_CUDA(cudaMemsetAsync(missing, 0, sizeof(int), c.s));
+    k_diag_pos<<<nblk(a.n), 256, 0, c.s>>>(a.rp, a.ci, a.n, diag.p, missing);
+    int h = 0;
+    MG_CUDA(cudaMemcpyAsync(&h, missing, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    if (h) throw Error(MPREC_SETUP, "AMG: structurally absent diagonal");
+}
+
+// rs_coarsen (amg.cpp:47-186): returns nc; fills cf (1 = C) and P
+static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<signed char>& cf, DCsr& p) {
+    const int n = a.n;
+    DBuf<double> mrow(n);
+    DBuf<int> scnt(n), stcnt(n), srp(n + 1), strp(n + 1), stfill(n);
+    MG_CUDA(cudaMemsetAsync(stcnt.p, 0, sizeof(int) * n, c.s));
+    MG_CUDA(cudaMemsetAsync(stfill.p, 0, sizeof(int) * n, c.s));
+    k_strength_count<<<nblk(n), 256, 0, c.s>>>(a.rp, a.ci, a.v, n, theta, mrow.p, scnt.p, stcnt.p);
+    const int ns = scan(c, s, scnt.p, srp.p, n);
+    scan(c, s, stcnt.p, strp.p, n);
+    DBuf<int> sci(std::max(ns, 1)), stci(std::max(ns, 1));
+    k_strength_fill<<<nblk(n), 256, 0, c.s>>>(a.rp, a.ci, a.v, n, theta, mrow.p, srp.p, sci.p, strp.p, stfill.p,
+                                              stci.p);
+    k_sort_rows<<<nblk(n), 256, 0, c.s>>>(strp.p, stci.p, nullptr, n);
+    check_launch("strength");
+
+    // ---- first pass: bucket queue
+    int lmax = 0;
+    {
+        DBuf<int> mx(1);
+        MG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), c.s));
+        k_max_int<<<std::min(nblk(n), 1024), 256, 0, c.s>>>(stcnt.p, n, mx.p);
+        MG_CUDA(cudaMemcpyAsync(&lmax, mx.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+    }
+    const int nbuckets = 2 * lmax + 1;
+    Buckets q;
+    q.n0 = (n + 63) / 64;
+    q.n1 = (q.n0 + 63) / 64;
+    q.n2 = (q.n1 + 63) / 64;
+    DBuf<unsigned long long> l0((size_t)nbuckets * q.n0), l1((size_t)nbuckets * q.n1), l2((size_t)nbuckets * q.n2);
+    DBuf<int> bcnt(nbuckets), lam(n), inc(n), jlist(n), klist(n);
+    MG_CUDA(cudaMemsetAsync(l0.p, 0, l0.bytes(), c.s));
+    MG_CUDA(cudaMemsetAsync(bcnt.p, 0, bcnt.bytes(), c.s));
+    MG_CUDA(cudaMemsetAsync(inc.p, 0, inc.bytes(), c.s));
+    q.l0 = l0.p;
+    q.l1 = l1.p;
+    q.l2 = l2.p;
+    q.cnt = bcnt.p;
+    cf.alloc(n);
+    signed char* mark = cf.p;
+    k_rs_init<<<nblk(n), 256, 0, c.s>>>(scnt.p, stcnt.p, n, mark, lam.p, q, nullptr);
+    k_bq_summary<<<nblk((int64_t)q.n1 * nbuckets), 256, 0, c.s>>>(l0.p, l1.p, q.n0, q.n1, nbuckets);
+    k_bq_summary<<<nblk((int64_t)q.n2 * nbuckets), 256, 0, c.s>>>(l1.p, l2.p, q.n1, q.n2, nbuckets);
+    {
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 0.0);
+        k_rs_select<<<1, 32, 0, c.s>>>(srp.p, sci.p, strp.p, stci.p, mark, lam.p, q, nbuckets, inc.p, jlist.p,
+                                       klist.p);
+        check_launch("rs first pass");
+    }
+    // ---- second pass
+    DBuf<int> flag(n), fpos(n + 1), list(n);
+    k_rs2_cand<<<nblk(n), 256, 0, c.s>>>(srp.p, sci.p, mark, n, flag.p);
+    int ncand = scan(c, s, flag.p, fpos.p, n);
+    if (ncand) {
+        k_compact<<<nblk(n), 256, 0, c.s>>>(flag.p, fpos.p, n, list.p);
+        k_rs2_seq<<<1, 32, 0, c.s>>>(srp.p, sci.p, mark, list.p, ncand);
+        check_launch("rs second pass");
+    }
+    // ---- third pass
+    k_rs3_cand<<<nblk(n), 256, 0, c.s>>>(srp.p, sci.p, mark, n, flag.p);
+    ncand = scan(c, s, flag.p, fpos.p, n);
+    if (ncand) {
+        k_compact<<<nblk(n), 256, 0, c.s>>>(flag.p, fpos.p, n, list.p);
+        k_rs3_seq<<<1, 32, 0, c.s>>>(srp.p, sci.p, mark, list.p, ncand);
+        check_launch("rs third pass");
+    }
+    // ---- coarse ids + direct interpolation
+    DBuf<int> isc(n), cpos(n + 1), pcnt(n);
+    k_is_c<<<nblk(n), 256, 0, c.s>>>(mark, n, isc.p);
+    const int nc = scan(c, s, isc.p, cpos.p, n);
+    k_interp<<<nblk(n), 256, 0, c.s>>>(a.rp, a.ci, a.v, n, theta, mrow.p, scnt.p, mark, cpos.p, 0, pcnt.p, nullptr,
+                                       nullptr, nullptr);
+    p.n = n;
+    p.m = nc;
+    p.rp.alloc(n + 1);
+    p.nnz = scan(c, s, pcnt.p, p.rp.p, n);
+    p.ci.alloc(std::max(p.nnz, 1));
+    p.v.alloc(std::max(p.nnz, 1));
+    k_interp<<<nblk(n), 256, 0, c.s>>>(a.rp, a.ci, a.v, n, theta, mrow.p, scnt.p, mark, cpos.p, 1, nullptr, p.rp.p,
+                                       p.ci.p, p.v.p);
+    check_launch("interp");
+    c.sync();
+    return nc;
+}
+
+// DenseFactor::factor + inverse for the coarsest level (dense_factor.cpp:7-19)
+static void coarse_factor(Ctx& c, const CsrView& a, DBuf<double>& lu, DBuf<double>& inv) {
+    const int n = a.n;
+    if (n > 20000) throw Error(MPREC_SETUP, "AMG coarsest level too large for the dense solve (" + std::to_string(n) + ")");
+    lu.alloc(std::max<int64_t>(1, (int64_t)n * n));
+    inv.alloc(std::max<int64_t>(1, (int64_t)n * n));
+    if (n == 0) return;
+    MG_CUDA(cudaMemsetAsync(lu.p, 0, lu.bytes(), c.s));
+    k_csr_to_dense<<<nblk(n), 256, 0, c.s>>>(a.rp, a.ci, a.v, n, lu.p);
+    DBuf<int> perm(n);
+    DBuf<double> scale(1);
+    {
+        Ctx::Scope sc(&c, MPREC_K_COARSE, 0.0);
+        k_dense_lu<<<1, 1024, 0, c.s>>>(lu.p, n, perm.p, scale.p);
+        check_launch("dense lu");
+    }
+    // pivot check |u_ii| <= 1e-14 * max|a|
+    std::vector<double> h = lu.to_host(c.s, (size_t)n * n);
+    double sc = 0.0;
+    MG_CUDA(cudaMemcpy(&sc, scale.p, sizeof(double), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i)
+        if (std::abs(h[(size_t)i * n + i]) <= 1e-14 * sc)
+            throw Error(MPREC_SINGULAR_BLOCK, "singular dense-factor pivot block in cell " + std::to_string(i), i);
+    k_dense_inv<<<nblk(n, 128), 128, 0, c.s>>>(lu.p, perm.p, n, inv.p);
+    check_launch("dense inverse");
+    c.sync();
+}
+
+// AMGHierarchy::setup (amg.cpp:188-214)
+void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p) {
+    prm = p;
+    lv.clear();
+    Scratch s;
+    auto L0 = std::make_unique<AmgLevel>();
+    L0->n = a0.n;
+    L0->a = a0;
+    if (!a0.diag) {
+        diag_positions(c, a0, L0->a_own.diag);
+        L0->a.diag = L0->a_own.diag.p;
+    }
+    lv.push_back(std::move(L0));
+    while (lv.back()->n > prm.max_coarse && int(lv.size()) < prm.max_levels) {
+        AmgLevel& f = *lv.back();
+        auto nl = std::make_unique<AmgLevel>();
+        const int nc = rs_coarsen(c, s, f.a, prm.theta, f.cf, nl->p);
+        if (nc == 0) {
+            f.cf.release();
+            break;
+        }
+        if (nc > int(0.95 * f.n))
+            throw Error(MPREC_SETUP, "AMG coarsening stagnated at size " + std::to_string(f.n));
+        transpose(c, s, nl->p, nl->r);
+        DCsr ap;
+        spgemm(c, s, f.a, nl->p.view(), ap);
+        spgemm(c, s, nl->r.view(), ap.view(), nl->a_own);
+        nl->n = nc;
+        nl->a = nl->a_own.view();
+        diag_positions(c, nl->a, nl->a_own.diag);
+        nl->a.diag = nl->a_own.diag.p;
+        lv.push_back(std::move(nl));
+    }
+    nco = lv.back()->n;
+    coarse_factor(c, lv.back()->a, coarse_lu, coarse_inv);
+    for (auto& l : lv) {
+        l->x.ensure(std::max(l->n, 1));
+        l->b.ensure(std::max(l->n, 1));
+        l->t.ensure(std::max(l->n, 1));
+        l->xf.ensure(std::max(l->n, 1));
+    }
+}
+
+}  // namespace mg

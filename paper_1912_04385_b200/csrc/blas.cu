@@ -1,0 +1,299 @@
+// blas.cu -- Ctx runtime + vector kernels of the Krylov loop (gmres.cpp:17-100):
+// deterministic fixed-order reductions (dot, norm), the fused MGS
+// dot/axpy step, scaling, multi-axpy, gathers and the stage combine.
+//
+// Reductions are deterministic: the grid size is a function of n only, each
+// block reduces a fixed grid-stride slice through a fixed shared-memory tree,
+// and the last block to finish sums the per-block partials in a fixed order.
+// Repeated solves are therefore bitwise identical (test_krylov.cpp:92-100).
+#include "mprec.cuh"
+
+namespace mg {
+
+// ============================================================== Ctx runtime ==
+Ctx::Ctx() {
+    MG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    int dev = 0;
+    MG_CUDA(cudaGetDevice(&dev));
+    MG_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+    red.alloc(kRedBlocks * 4);
+    red_ctr.alloc(64);
+    MG_CUDA(cudaMemsetAsync(red_ctr.p, 0, red_ctr.bytes(), s));
+    scal.alloc(4096);
+    counters.alloc(64);
+    err.alloc(64);
+}
+
+Ctx::~Ctx() {
+    if (s) cudaStreamSynchronize(s);
+    for (auto& p : pending) {
+        event_pool.push_back(p.a);
+        event_pool.push_back(p.b);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (s) cudaStreamDestroy(s);
+}
+
+cudaEvent_t Ctx::get_event() {
+    if (!event_pool.empty()) {
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    MG_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+Ctx::Scope::Scope(Ctx* c_, int kc_, double bytes_) : c(c_), kc(kc_), bytes(bytes_) {
+    c->launches++;
+    if (c->profile) {
+        a = c->get_event();
+        cudaEventRecord(a, c->s);
+    }
+}
+
+Ctx::Scope::~Scope() {
+    if (a) {
+        cudaEvent_t b = c->get_event();
+        cudaEventRecord(b, c->s);
+        c->pending.push_back({kc, bytes, a, b});
+        if (c->pending.size() > 4096) c->harvest();
+    } else {
+        c->stat[kc].launches++;
+        c->stat[kc].bytes += bytes;
+    }
+}
+
+void Ctx::harvest() {
+    if (pending.empty()) return;
+    MG_CUDA(cudaStreamSynchronize(s));
+    for (auto& p : pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        stat[p.kc].ms += ms;
+        stat[p.kc].launches++;
+        stat[p.kc].bytes += p.bytes;
+        event_pool.push_back(p.a);
+        event_pool.push_back(p.b);
+    }
+    pending.clear();
+}
+
+// ================================================================== kernels ==
+namespace {
+
+constexpr int kRT = 256;  // reduction block size
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = kRT / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    return sh[0];
+}
+
+// Final stage of a two-level reduction, run by the last block to arrive.
+// mode bit0: sqrt of the sum; bit1: accumulate into *hsum too.
+__device__ void finish(double part, double* partials, unsigned* ctr, double* out, double* hsum, int mode,
+                       double* sh) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = part;
+        __threadfence();
+        const unsigned t = atomicInc(ctr, 0xFFFFFFFFu);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double v = 0.0;
+    for (int i = threadIdx.x; i < gridDim.x; i += kRT) v += ((volatile double*)partials)[i];
+    const double tot = block_sum(v, sh);
+    if (threadIdx.x == 0) {
+        const double r = (mode & 1) ? sqrt(tot) : tot;
+        *out = r;
+        if (hsum) *hsum += r;
+        *ctr = 0;
+    }
+}
+
+__global__ void k_fill(double* x, double v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void k_fill_bits(unsigned long long* x, unsigned long long v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void k_copy(double* y, const double* x, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i];
+}
+
+__global__ void __launch_bounds__(kRT) k_dot(const double* a, const double* b, int64_t n, double* partials,
+                                             unsigned* ctr, double* out, int mode) {
+    __shared__ double sh[kRT];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)kRT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRT)
+        s += a[i] * b[i];
+    const double part = block_sum(s, sh);
+    __syncthreads();
+    finish(part, partials, ctr, out, nullptr, mode, sh);
+}
+
+// w -= (*hprev) * vprev ; partial of vcur . w  (vcur == w: squared norm)
+__global__ void __launch_bounds__(kRT) k_mgs(double* w, const double* vprev, const double* hprev,
+                                             const double* vcur, int64_t n, double* partials, unsigned* ctr,
+                                             double* hout, double* hsum, int mode, const int* gate) {
+    if (gate && *gate == 0) return;
+    __shared__ double sh[kRT];
+    const double h = vprev ? *hprev : 0.0;
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)kRT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRT) {
+        double wi = w[i];
+        if (vprev) {
+            wi = wi - h * vprev[i];
+            w[i] = wi;
+        }
+        if (vcur) s += vcur[i] * wi;
+    }
+    if (!vcur) return;
+    const double part = block_sum(s, sh);
+    __syncthreads();
+    finish(part, partials, ctr, hout, hsum, mode, sh);
+}
+
+__global__ void k_gate(const double* wnorm, const double* prenorm, int* gate) {
+    *gate = (*wnorm < 0.7 * *prenorm) ? 1 : 0;
+}
+
+__global__ void k_div(double* y, const double* x, double a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i] / a;
+}
+
+__global__ void k_multi_axpy(double* z, const double* const* vt, const double* y, int k, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < k; ++j) acc += y[j] * vt[j][i];
+        z[i] = acc;
+    }
+}
+
+__global__ void k_sub(double* out, const double* b, const double* ax, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = b[i] - ax[i];
+}
+
+__global__ void k_gather(double* out, const double* x, int nc, int stride, int f) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x)
+        out[i] = x[(int64_t)i * stride + f];
+}
+
+__global__ void k_combine(double* y, const double* w, const double* xs, int fx, const double* vs, int fv, int nc,
+                          int nb) {
+    const int64_t n = (int64_t)nc * nb;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = int(i / nb), f = int(i - (int64_t)c * nb);
+        double s = 0.0;
+        if (xs && f == fx) s = xs[c];
+        if (vs && f == fv) s = s + vs[c];
+        y[i] = s + w[i];
+    }
+}
+
+inline int red_grid(int64_t n) {
+    int64_t g = (n + kRT - 1) / kRT;
+    return int(std::max<int64_t>(1, std::min<int64_t>(g, kRedBlocks)));
+}
+
+}  // namespace
+
+void fill(Ctx& c, double* x, double v, int64_t n) {
+    if (n <= 0) return;
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * n);
+    k_fill<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(x, v, n);
+    check_launch("fill");
+}
+
+void fill_pending(Ctx& c, double* x, int64_t n) {
+    if (n <= 0) return;
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * n);
+    k_fill_bits<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>((unsigned long long*)x, kPending, n);
+    check_launch("fill_pending");
+}
+
+void copy(Ctx& c, double* y, const double* x, int64_t n) {
+    if (n <= 0) return;
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * n);
+    k_copy<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(y, x, n);
+    check_launch("copy");
+}
+
+void dot(Ctx& c, const double* a, const double* b, int64_t n, double* out) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * n);
+    k_dot<<<red_grid(n), kRT, 0, c.s>>>(a, b, n, c.red.p, c.red_ctr.p, out, 0);
+    check_launch("dot");
+}
+
+void nrm2(Ctx& c, const double* a, int64_t n, double* out) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * n);
+    k_dot<<<red_grid(n), kRT, 0, c.s>>>(a, a, n, c.red.p, c.red_ctr.p, out, 1);
+    check_launch("nrm2");
+}
+
+void mgs_step(Ctx& c, double* w, const double* vprev, const double* hprev, const double* vcur, int64_t n,
+              double* hout, bool accumulate, double* hsum, const int* gate) {
+    const bool self = (vcur == w);
+    double bytes = 8.0 * n * ((vprev ? 3 : 1) + (vcur && !self ? 1 : 0));
+    Ctx::Scope sc(&c, MPREC_K_MGS, bytes);
+    const int mode = self ? 1 : 0;
+    k_mgs<<<red_grid(n), kRT, 0, c.s>>>(w, vprev, hprev, vcur, n, c.red.p, c.red_ctr.p, hout,
+                                          accumulate ? hsum : nullptr, mode, gate);
+    check_launch("mgs_step");
+}
+
+void set_reorth_gate(Ctx& c, const double* wnorm, const double* prenorm, int* gate) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 0.0);
+    k_gate<<<1, 1, 0, c.s>>>(wnorm, prenorm, gate);
+    check_launch("gate");
+}
+
+void div_scalar(Ctx& c, double* y, const double* x, double a, int64_t n) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * n);
+    k_div<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(y, x, a, n);
+    check_launch("div");
+}
+
+void multi_axpy(Ctx& c, double* z, const double* const* vt, const double* y, int k, int64_t n) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * n * (k + 1));
+    k_multi_axpy<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(z, vt, y, k, n);
+    check_launch("multi_axpy");
+}
+
+void sub(Ctx& c, double* out, const double* b, const double* ax, int64_t n) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 24.0 * n);
+    k_sub<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(out, b, ax, n);
+    check_launch("sub");
+}
+
+void gather_stride(Ctx& c, double* out, const double* x, int nc, int stride, int f) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * nc);
+    k_gather<<<grid_for(nc, 256, c.sm_count * 8), 256, 0, c.s>>>(out, x, nc, stride, f);
+    check_launch("gather");
+}
+
+void stage_combine(Ctx& c, double* y, const double* w, const double* xs, int fx, const double* vs, int fv, int nc,
+                   int nb) {
+    const int64_t n = (int64_t)nc * nb;
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * n + 8.0 * nc * ((xs ? 1 : 0) + (vs ? 1 : 0)));
+    k_combine<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(y, w, xs, fx, vs, fv, nc, nb);
+    check_launch("combine");
+}
+
+}  // namespace mg

@@ -1,0 +1,789 @@
+// capi.cu -- the C ABI of include/mprec_gpu.h: system handles, the staged
+// right preconditioner (StagePreconditioner::apply, stages.cpp:36-59), the
+// GMRES host loop over device vectors (gmres.cpp:8-106) and solve_system's
+// tolerance-tightening retries (harness.cpp:190-219).
+//
+// Everything numeric runs in the sm_100a kernels of this library; the host
+// only keeps the (max_iter+1) x max_iter Hessenberg matrix and the Givens
+// rotations, exactly as the reference does, reading one Hessenberg column
+// (k+2 doubles) back per iteration.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+
+#include "mprec.cuh"
+
+using namespace mg;
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_payload = -1;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return MPREC_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        g_payload = e.payload;
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = "host allocation failed";
+        g_payload = -1;
+        return MPREC_INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        g_payload = -1;
+        return MPREC_INTERNAL;
+    }
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Validates a canonical BSR (block_matrix.cpp:32-69 invariants) and uploads the pattern.
+void load_pattern(Ctx& c, Pattern& p, int nc, int nb, const int* rp, const int* ci) {
+    if (nc < 1) throw Error(MPREC_DIMENSION, "layout needs at least one cell");
+    if (nb < 1) throw Error(MPREC_DIMENSION, "block size must be >= 1");
+    if (!rp || !ci) throw Error(MPREC_DIMENSION, "null pattern");
+    if (rp[0] != 0) throw Error(MPREC_INDEX, "row_ptr[0] must be 0");
+    p.nc = nc;
+    p.nnzb = rp[nc];
+    p.h_rp.assign(rp, rp + nc + 1);
+    p.h_ci.assign(ci, ci + p.nnzb);
+    p.h_dpos.assign(nc, -1);
+    for (int r = 0; r < nc; ++r) {
+        if (rp[r + 1] < rp[r]) throw Error(MPREC_INDEX, "row_ptr not monotone");
+        for (int k = rp[r]; k < rp[r + 1]; ++k) {
+            if (ci[k] < 0 || ci[k] >= nc) throw Error(MPREC_INDEX, "block column out of range");
+            if (k > rp[r] && ci[k] <= ci[k - 1]) throw Error(MPREC_INDEX, "block columns not sorted");
+            if (ci[k] == r) p.h_dpos[r] = k;
+        }
+        if (p.h_dpos[r] < 0)
+            throw Error(MPREC_DIMENSION, "diagonal block missing in cell " + std::to_string(r), r);
+    }
+    p.rp.upload(p.h_rp.data(), p.h_rp.size(), c.s);
+    p.ci.upload(p.h_ci.data(), std::max<size_t>(p.h_ci.size(), 1), c.s);
+    p.dpos.upload(p.h_dpos.data(), p.h_dpos.size(), c.s);
+}
+
+BsrView view_of(const Pattern& p, int nb, double* val) {
+    BsrView v;
+    v.nc = p.nc;
+    v.nb = nb;
+    v.nnzb = p.nnzb;
+    v.rp = p.rp.p;
+    v.ci = p.ci.p;
+    v.dpos = p.dpos.p;
+    v.val = val;
+    return v;
+}
+
+using DevOp = std::function<void(const double* x, double* y)>;
+
+struct GmresOut {
+    int iterations = 0;
+    bool converged = false, breakdown = false;
+    std::vector<double> history;
+    double final_true_residual = 0.0;
+};
+
+// Krylov basis allocated lazily in chunks (at c5 one vector is 256 MB).
+struct Basis {
+    int64_t n = 0;
+    int chunk = 8;
+    std::vector<DBuf<double>> blocks;
+    double* vec(int i) {
+        const int b = i / chunk;
+        while (int(blocks.size()) <= b) blocks.emplace_back(size_t(n) * chunk);
+        return blocks[b].p + int64_t(i % chunk) * n;
+    }
+};
+
+struct Krylov {
+    Basis V;
+    DBuf<double> w, t, hcol, cre;
+    DBuf<const double*> vtab;
+    DBuf<double> ydev;
+};
+
+// gmres.cpp:8-106 over device vectors.  b, x: device; n unknowns.
+GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M, const double* b, double tol,
+                   int max_iter, double* x) {
+    if (tol <= 0.0) throw Error(MPREC_DIMENSION, "gmres: tolerance must be positive");
+    GmresOut out;
+    double* sc = c.scal.p;  // [0] bnorm [1] pre_norm [2] wn [3] norm after reorth
+    nrm2(c, b, n, sc + 0);
+    double bnorm = 0.0;
+    MG_CUDA(cudaMemcpyAsync(&bnorm, sc + 0, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    if (bnorm == 0.0) {
+        fill(c, x, 0.0, n);
+        out.converged = true;
+        out.history.push_back(0.0);
+        return out;
+    }
+    const int max_it = int(std::min<int64_t>(max_iter, n));
+    kr.V.n = n;
+    kr.w.ensure(n);
+    kr.t.ensure(n);
+    kr.hcol.ensure(max_it + 2);
+    kr.cre.ensure(max_it + 2);
+    int* gate = c.err.p + 8;
+    div_scalar(c, kr.V.vec(0), b, bnorm, n);
+    const int ld = max_it + 1;
+    std::vector<double> h(size_t(ld) * std::max(max_it, 1), 0.0), cs(max_it), sn(max_it), g(max_it + 1, 0.0);
+    auto H = [&](int i, int j) -> double& { return h[size_t(j) * ld + i]; };
+    g[0] = bnorm;
+    out.history.push_back(1.0);
+    std::vector<double> col(max_it + 4);
+    int k = 0;
+    for (; k < max_it; ++k) {
+        double* vk = kr.V.vec(k);
+        M(vk, kr.t.p);
+        A(kr.t.p, kr.w.p);
+        double* w = kr.w.p;
+        double* hc = kr.hcol.p;
+        double* cr = kr.cre.p;
+        nrm2(c, w, n, sc + 1);
+        // MGS (gmres.cpp:39-42), axpy of step i fused with the dot of step i+1
+        mgs_step(c, w, nullptr, nullptr, kr.V.vec(0), n, hc + 0, false, nullptr, nullptr);
+        for (int i = 1; i <= k; ++i)
+            mgs_step(c, w, kr.V.vec(i - 1), hc + i - 1, kr.V.vec(i), n, hc + i, false, nullptr, nullptr);
+        mgs_step(c, w, vk, hc + k, w, n, sc + 2, false, nullptr, nullptr);  // w -= h_kk v_k ; ||w||
+        // one re-orthogonalisation pass when ||w|| < 0.7 pre_norm (gmres.cpp:44-50), gated on device
+        set_reorth_gate(c, sc + 2, sc + 1, gate);
+        mgs_step(c, w, nullptr, nullptr, kr.V.vec(0), n, cr + 0, true, hc + 0, gate);
+        for (int i = 1; i <= k; ++i)
+            mgs_step(c, w, kr.V.vec(i - 1), cr + i - 1, kr.V.vec(i), n, cr + i, true, hc + i, gate);
+        mgs_step(c, w, vk, cr + k, w, n, sc + 3, false, nullptr, gate);
+        // read back the Hessenberg column
+        MG_CUDA(cudaMemcpyAsync(col.data(), hc, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c.s));
+        double tail[3];
+        int gh = 0;
+        MG_CUDA(cudaMemcpyAsync(tail, sc + 1, sizeof(double) * 3, cudaMemcpyDeviceToHost, c.s));
+        MG_CUDA(cudaMemcpyAsync(&gh, gate, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        for (int i = 0; i <= k; ++i) H(i, k) = col[i];
+        H(k + 1, k) = gh ? tail[2] : tail[1];
+        const double subdiag = H(k + 1, k);
+        for (int i = 0; i < k; ++i) {
+            const double tt = cs[i] * H(i, k) + sn[i] * H(i + 1, k);
+            H(i + 1, k) = -sn[i] * H(i, k) + cs[i] * H(i + 1, k);
+            H(i, k) = tt;
+        }
+        const double denom = std::hypot(H(k, k), H(k + 1, k));
+        if (denom == 0.0) {
+            out.breakdown = true;
+            ++k;
+            break;
+        }
+        cs[k] = H(k, k) / denom;
+        sn[k] = H(k + 1, k) / denom;
+        H(k, k) = denom;
+        H(k + 1, k) = 0.0;
+        g[k + 1] = -sn[k] * g[k];
+        g[k] = cs[k] * g[k];
+        const double rel = std::abs(g[k + 1]) / bnorm;
+        out.history.push_back(rel);
+        if (rel <= tol) {
+            ++k;
+            break;
+        }
+        if (subdiag == 0.0) {
+            out.breakdown = true;
+            ++k;
+            break;
+        }
+        div_scalar(c, kr.V.vec(k + 1), w, subdiag, n);
+    }
+    out.iterations = k;
+    if (k > 0) {
+        std::vector<double> y(k, 0.0);
+        for (int i = k - 1; i >= 0; --i) {
+            double acc = g[i];
+            for (int j = i + 1; j < k; ++j) acc -= H(i, j) * y[j];
+            y[i] = acc / H(i, i);
+        }
+        std::vector<const double*> tab(k);
+        for (int i = 0; i < k; ++i) tab[i] = kr.V.vec(i);
+        kr.vtab.ensure(k);
+        kr.ydev.ensure(k);
+        kr.vtab.upload(tab.data(), k, c.s);
+        kr.ydev.upload(y.data(), k, c.s);
+        multi_axpy(c, kr.w.p, kr.vtab.p, kr.ydev.p, k, n);
+        M(kr.w.p, x);
+        c.sync();  // the host vectors above must outlive the async uploads
+    } else {
+        fill(c, x, 0.0, n);
+    }
+    A(x, kr.t.p);
+    sub(c, kr.t.p, b, kr.t.p, n);
+    nrm2(c, kr.t.p, n, sc + 0);
+    double rn = 0.0;
+    MG_CUDA(cudaMemcpyAsync(&rn, sc + 0, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    out.final_true_residual = rn / bnorm;
+    out.converged = out.history.back() <= tol || out.final_true_residual <= tol;
+    return out;
+}
+
+void fill_result(mprec_solve_result* r, const GmresOut& g, int attempts, double setup_s, double solve_s,
+                 double* history, int cap) {
+    if (!r) return;
+    r->iterations = g.iterations;
+    r->converged = g.converged;
+    r->breakdown = g.breakdown;
+    r->attempts = attempts;
+    r->final_true_residual = g.final_true_residual;
+    r->setup_s = setup_s;
+    r->solve_s = solve_s;
+    int nh = int(g.history.size());
+    if (history && cap < nh) nh = cap;
+    if (history)
+        for (int i = 0; i < nh; ++i) history[i] = g.history[i];
+    r->history_len = history ? nh : int(g.history.size());
+}
+
+}  // namespace
+
+// ============================================================ AMG handle ==
+struct mprec_gpu_amg {
+    Ctx* ctx = nullptr;
+    std::unique_ptr<Ctx> own_ctx;
+    Amg* amg = nullptr;
+    std::unique_ptr<Amg> own_amg;
+    DCsr a0;
+    DBuf<double> r, x;
+};
+
+// ============================================================ ILU handle ==
+struct mprec_gpu_ilu {
+    Ctx ctx;
+    Pattern pat;
+    Ilu ilu;
+    DBuf<double> vals, r, y;
+};
+
+// ========================================================= system handle ==
+struct mprec_gpu_system {
+    Ctx ctx;
+    Pattern pat;
+    int nb = 0;
+    int64_t n = 0;
+    DBuf<double> a_val, abar_val, lu_val, b, bbar, fP, fT;
+    std::unique_ptr<Amg> amgT, amgP;
+    Ilu ilu;
+    int method = -1;
+    bool ready = false;
+    double setup_s = 0.0;
+    // work vectors of the stage preconditioner
+    DBuf<double> gT, xT, gP, vP, z, u, w, x, r, y;
+    Krylov kr;
+    std::vector<std::unique_ptr<mprec_gpu_amg>> views;
+
+    BsrView A() { return view_of(pat, nb, a_val.p); }
+    BsrView Abar() { return view_of(pat, nb, abar_val.p); }
+    int P() const { return nb - 2; }
+    int T() const { return nb - 1; }
+
+    // StagePreconditioner::apply (stages.cpp:36-59), device pointers
+    void prec_apply(const double* rin, double* yout) {
+        Ctx& c = ctx;
+        const int nc = pat.nc;
+        if (method == MPREC_METHOD_ILU0) {
+            ilu.apply(c, rin, yout);
+        } else if (method == MPREC_METHOD_CPR_AMG) {
+            gather_stride(c, gP.p, rin, nc, nb, P());
+            amgP->apply(c, gP.p, vP.p);
+            bsr_col_update(c, Abar(), P(), vP.p, rin, z.p, nullptr, 0);
+            ilu.apply(c, z.p, w.p);
+            stage_combine(c, yout, w.p, nullptr, 0, vP.p, P(), nc, nb);
+        } else {
+            gather_stride(c, gT.p, rin, nc, nb, T());
+            amgT->apply(c, gT.p, xT.p);
+            bsr_col_update(c, Abar(), T(), xT.p, rin, z.p, gP.p, P());
+            amgP->apply(c, gP.p, vP.p);
+            bsr_col_update(c, Abar(), P(), vP.p, z.p, u.p, nullptr, 0);
+            ilu.apply(c, u.p, w.p);
+            stage_combine(c, yout, w.p, xT.p, T(), vP.p, P(), nc, nb);
+        }
+    }
+
+    // Stage::apply (stages.cpp:25-34) for stage i, full vectors
+    void stage_apply(int i, const double* rin, double* yout) {
+        Ctx& c = ctx;
+        const int nc = pat.nc;
+        const int nst = method == MPREC_METHOD_CPTR3_AMG ? 3 : (method == MPREC_METHOD_CPR_AMG ? 2 : 1);
+        if (i < 0 || i >= nst) throw Error(MPREC_INDEX, "stage out of range");
+        if (i == nst - 1) {
+            ilu.apply(c, rin, yout);
+            return;
+        }
+        Amg* a = nullptr;
+        int f = 0;
+        if (method == MPREC_METHOD_CPR_AMG) {
+            a = amgP.get();
+            f = P();
+        } else if (i == 0) {
+            a = amgT.get();
+            f = T();
+        } else {
+            a = amgP.get();
+            f = P();
+        }
+        gather_stride(c, gT.p, rin, nc, nb, f);
+        a->apply(c, gT.p, xT.p);
+        fill(c, w.p, 0.0, n);
+        stage_combine(c, yout, w.p, xT.p, f, nullptr, 0, nc, nb);
+    }
+
+    GmresOut solve_attempts(double tol, int max_iter, double* xdev, int* attempts) {
+        Ctx& c = ctx;
+        const DevOp Aop = [this](const double* xx, double* yy) { bsr_spmv(ctx, Abar(), xx, yy, nullptr, MPREC_K_SPMV); };
+        const DevOp Mop = [this](const double* xx, double* yy) { prec_apply(xx, yy); };
+        double bn = 0.0;
+        nrm2(c, b.p, n, c.scal.p + 8);
+        MG_CUDA(cudaMemcpyAsync(&bn, c.scal.p + 8, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+        double opt_tol = tol;
+        GmresOut res;
+        *attempts = 0;
+        for (int attempt = 0; attempt < 3; ++attempt) {
+            ++*attempts;
+            res = gmres_dev(c, kr, n, Aop, Mop, bbar.p, opt_tol, max_iter, xdev);
+            // residual_check on the ORIGINAL system (gmres.cpp:108-112)
+            bsr_spmv(c, A(), xdev, kr.t.p, bn == 0.0 ? nullptr : b.p, MPREC_K_SPMV);
+            nrm2(c, kr.t.p, n, c.scal.p + 9);
+            double rn = 0.0;
+            MG_CUDA(cudaMemcpyAsync(&rn, c.scal.p + 9, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+            c.sync();
+            res.final_true_residual = bn == 0.0 ? rn : rn / bn;
+            if (!res.converged || res.final_true_residual <= tol) break;
+            opt_tol *= 0.5 * tol / res.final_true_residual;
+        }
+        if (res.converged && res.final_true_residual > tol) res.converged = false;
+        return res;
+    }
+};
+
+extern "C" {
+
+const char* mprec_gpu_last_error(void) { return g_err.c_str(); }
+int mprec_gpu_error_payload(void) { return g_payload; }
+
+int mprec_gpu_device_info(int* sm, int* major, int* minor, int64_t* mem) {
+    return guard([&] {
+        int dev = 0, cnt = 0;
+        MG_CUDA(cudaGetDeviceCount(&cnt));
+        if (cnt < 1) throw Error(MPREC_CUDA, "no CUDA device");
+        MG_CUDA(cudaGetDevice(&dev));
+        cudaDeviceProp p;
+        MG_CUDA(cudaGetDeviceProperties(&p, dev));
+        if (sm) *sm = p.multiProcessorCount;
+        if (major) *major = p.major;
+        if (minor) *minor = p.minor;
+        if (mem) *mem = int64_t(p.totalGlobalMem);
+    });
+}
+
+int mprec_gpu_create(const mprec_bsr* a, mprec_gpu_system** out) {
+    return guard([&] {
+        if (!a || !out) throw Error(MPREC_DIMENSION, "null argument");
+        auto h = std::make_unique<mprec_gpu_system>();
+        load_pattern(h->ctx, h->pat, a->n_cells, a->nb, a->row_ptr, a->col_idx);
+        h->nb = a->nb;
+        h->n = int64_t(a->n_cells) * a->nb;
+        h->a_val.upload(a->values, std::max<size_t>(size_t(h->pat.nnzb) * a->nb * a->nb, 1), h->ctx.s);
+        h->ctx.sync();
+        *out = h.release();
+    });
+}
+
+int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg, const double* b) {
+    return guard([&] {
+        if (!h) throw Error(MPREC_DIMENSION, "null handle");
+        if (method != MPREC_METHOD_ILU0 && method != MPREC_METHOD_CPR_AMG && method != MPREC_METHOD_CPTR3_AMG)
+            throw Error(MPREC_CONFIG, "unknown method id " + std::to_string(method));
+        if (method != MPREC_METHOD_ILU0 && h->nb < 2)
+            throw Error(MPREC_DIMENSION, "CPR/CPTR3 need P and T unknowns (nb >= 2)");
+        Ctx& c = h->ctx;
+        h->ready = false;
+        const double t0 = now_s();
+        const int64_t n = h->n;
+        const size_t nv = size_t(h->pat.nnzb) * h->nb * h->nb;
+        h->b.upload(b, n, c.s);
+        h->bbar.ensure(n);
+        copy(c, h->bbar.p, h->b.p, n);
+        h->abar_val.ensure(nv);
+        MG_CUDA(cudaMemcpyAsync(h->abar_val.p, h->a_val.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.s));
+        // left_scale (scaling.cpp:149-158)
+        left_scale(c, h->Abar(), h->bbar.p, method);
+        // build_preconditioner (stages.cpp:129-138)
+        AmgParams prm;
+        if (amg) {
+            prm.theta = amg->strength_threshold;
+            prm.max_coarse = amg->max_coarse_size;
+            prm.max_levels = amg->max_levels;
+        }
+        const int nc = h->pat.nc;
+        h->views.clear();
+        h->amgT.reset();
+        h->amgP.reset();
+        if (method == MPREC_METHOD_CPTR3_AMG) {
+            h->fT.ensure(h->pat.nnzb);
+            extract_field(c, h->Abar(), h->T(), h->fT.p);
+            CsrView a0{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fT.p, h->pat.dpos.p};
+            h->amgT = std::make_unique<Amg>();
+            h->amgT->setup(c, a0, prm);
+        }
+        if (method != MPREC_METHOD_ILU0) {
+            h->fP.ensure(h->pat.nnzb);
+            extract_field(c, h->Abar(), h->P(), h->fP.p);
+            CsrView a0{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fP.p, h->pat.dpos.p};
+            h->amgP = std::make_unique<Amg>();
+            h->amgP->setup(c, a0, prm);
+        }
+        // ILU(0) of Ā
+        h->lu_val.ensure(nv);
+        MG_CUDA(cudaMemcpyAsync(h->lu_val.p, h->abar_val.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.s));
+        h->ilu.lu = view_of(h->pat, h->nb, h->lu_val.p);
+        h->ilu.pat = &h->pat;
+        h->ilu.factor(c);
+        for (DBuf<double>* v : {&h->gT, &h->xT, &h->gP, &h->vP}) v->ensure(nc);
+        for (DBuf<double>* v : {&h->z, &h->u, &h->w, &h->x, &h->r, &h->y}) v->ensure(n);
+        c.sync();
+        h->method = method;
+        h->ready = true;
+        h->setup_s = now_s() - t0;
+    });
+}
+
+int mprec_gpu_apply(mprec_gpu_system* h, const double* r, double* z) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        h->r.upload(r, h->n, h->ctx.s);
+        h->prec_apply(h->r.p, h->y.p);
+        h->y.download(z, h->n, h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_apply_stage(mprec_gpu_system* h, int stage, const double* r, double* z) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        h->r.upload(r, h->n, h->ctx.s);
+        h->stage_apply(stage, h->r.p, h->y.p);
+        h->y.download(z, h->n, h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_spmv(mprec_gpu_system* h, int which, const double* x, double* y) {
+    return guard([&] {
+        if (!h) throw Error(MPREC_DIMENSION, "null handle");
+        if (which != 0 && !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        h->r.ensure(h->n);
+        h->y.ensure(h->n);
+        h->r.upload(x, h->n, h->ctx.s);
+        bsr_spmv(h->ctx, which == 0 ? h->A() : h->Abar(), h->r.p, h->y.p, nullptr, MPREC_K_SPMV);
+        h->y.download(y, h->n, h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_solve_dev(mprec_gpu_system* h, double tol, int max_iter, double* x_dev, mprec_solve_result* out) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        const double t0 = now_s();
+        int attempts = 0;
+        double* xd = x_dev ? x_dev : h->x.p;
+        const GmresOut g = h->solve_attempts(tol, max_iter, xd, &attempts);
+        h->ctx.sync();
+        fill_result(out, g, attempts, h->setup_s, now_s() - t0, nullptr, 0);
+    });
+}
+
+int mprec_gpu_solve(mprec_gpu_system* h, double tol, int max_iter, double* x, mprec_solve_result* out,
+                    double* history, int history_cap) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        const double t0 = now_s();
+        int attempts = 0;
+        const GmresOut g = h->solve_attempts(tol, max_iter, h->x.p, &attempts);
+        h->x.download(x, h->n, h->ctx.s);
+        h->ctx.sync();
+        fill_result(out, g, attempts, h->setup_s, now_s() - t0, history, history_cap);
+    });
+}
+
+int mprec_gpu_solve_system(const mprec_bsr* a, const double* b, int method, double tol, int max_iter, double* x,
+                           mprec_solve_result* out) {
+    mprec_gpu_system* h = nullptr;
+    int st = mprec_gpu_create(a, &h);
+    if (st == MPREC_OK) st = mprec_gpu_setup(h, method, nullptr, b);
+    if (st == MPREC_OK) st = mprec_gpu_solve(h, tol, max_iter, x, out, nullptr, 0);
+    if (h) {
+        std::string keep = g_err;
+        int kp = g_payload;
+        mprec_gpu_destroy(h);
+        g_err = keep;
+        g_payload = kp;
+    }
+    return st;
+}
+
+int mprec_gpu_get_scaled(mprec_gpu_system* h, double* abar, double* bbar) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        if (abar) h->abar_val.download(abar, size_t(h->pat.nnzb) * h->nb * h->nb, h->ctx.s);
+        if (bbar) h->bbar.download(bbar, h->n, h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_get_ilu(mprec_gpu_system* h, double* lu) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        h->lu_val.download(lu, size_t(h->pat.nnzb) * h->nb * h->nb, h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_n_stages(mprec_gpu_system* h, int* n) {
+    return guard([&] {
+        if (!h) throw Error(MPREC_DIMENSION, "null handle");
+        *n = !h->ready ? 0 : (h->method == MPREC_METHOD_CPTR3_AMG ? 3 : (h->method == MPREC_METHOD_CPR_AMG ? 2 : 1));
+    });
+}
+
+int mprec_gpu_stage_amg(mprec_gpu_system* h, int stage, mprec_gpu_amg** out) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        Amg* a = nullptr;
+        if (h->method == MPREC_METHOD_CPR_AMG && stage == 0) a = h->amgP.get();
+        if (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) a = h->amgT.get();
+        if (h->method == MPREC_METHOD_CPTR3_AMG && stage == 1) a = h->amgP.get();
+        if (!a) throw Error(MPREC_INDEX, "not an AMG stage");
+        auto v = std::make_unique<mprec_gpu_amg>();
+        v->ctx = &h->ctx;
+        v->amg = a;
+        *out = v.get();
+        h->views.push_back(std::move(v));
+    });
+}
+
+void mprec_gpu_destroy(mprec_gpu_system* h) {
+    if (!h) return;
+    try {
+        h->ctx.sync();
+    } catch (...) {
+    }
+    delete h;
+}
+
+// ------------------------------------------------------------------ AMG ---
+int mprec_gpu_amg_create(const mprec_csr* a, const mprec_amg_params* p, mprec_gpu_amg** out) {
+    return guard([&] {
+        if (!a || !out) throw Error(MPREC_DIMENSION, "null argument");
+        const int n = a->n_rows;
+        if (n < 0) throw Error(MPREC_DIMENSION, "negative matrix dimension");
+        const int nnz = a->row_ptr[n];
+        for (int i = 0; i < n; ++i)
+            for (int k = a->row_ptr[i]; k < a->row_ptr[i + 1]; ++k) {
+                if (a->col_idx[k] < 0 || a->col_idx[k] >= n) throw Error(MPREC_INDEX, "column out of range");
+                if (k > a->row_ptr[i] && a->col_idx[k] <= a->col_idx[k - 1])
+                    throw Error(MPREC_INDEX, "CSR not canonical (columns must be strictly increasing)");
+            }
+        auto h = std::make_unique<mprec_gpu_amg>();
+        h->own_ctx = std::make_unique<Ctx>();
+        h->ctx = h->own_ctx.get();
+        Ctx& c = *h->ctx;
+        h->a0.n = h->a0.m = n;
+        h->a0.nnz = nnz;
+        h->a0.rp.upload(a->row_ptr, n + 1, c.s);
+        h->a0.ci.upload(a->col_idx, std::max(nnz, 1), c.s);
+        h->a0.v.upload(a->values, std::max(nnz, 1), c.s);
+        AmgParams prm;
+        if (p) {
+            prm.theta = p->strength_threshold;
+            prm.max_coarse = p->max_coarse_size;
+            prm.max_levels = p->max_levels;
+        }
+        h->own_amg = std::make_unique<Amg>();
+        h->amg = h->own_amg.get();
+        CsrView v = h->a0.view();
+        v.diag = nullptr;
+        h->amg->setup(c, v, prm);
+        c.sync();
+        *out = h.release();
+    });
+}
+
+int mprec_gpu_amg_apply(mprec_gpu_amg* h, const double* r, double* x) {
+    return guard([&] {
+        Ctx& c = *h->ctx;
+        const int n = h->amg->lv[0]->n;
+        h->r.upload(r, std::max(n, 1), c.s);
+        h->x.ensure(std::max(n, 1));
+        h->amg->apply(c, h->r.p, h->x.p);
+        h->x.download(x, n, c.s);
+        c.sync();
+    });
+}
+
+int mprec_gpu_amg_n_levels(mprec_gpu_amg* h, int* n) {
+    return guard([&] { *n = h->amg->n_levels(); });
+}
+
+int mprec_gpu_amg_level_info(mprec_gpu_amg* h, int l, int* n, int* nnz_a, int* nnz_p) {
+    return guard([&] {
+        if (l < 0 || l >= h->amg->n_levels()) throw Error(MPREC_INDEX, "level out of range");
+        const AmgLevel& L = *h->amg->lv[l];
+        *n = L.n;
+        *nnz_a = L.a.nnz;
+        *nnz_p = l == 0 ? 0 : L.p.nnz;
+    });
+}
+
+int mprec_gpu_amg_get_csr(mprec_gpu_amg* h, int l, int which, int* rp, int* ci, double* v) {
+    return guard([&] {
+        if (l < 0 || l >= h->amg->n_levels()) throw Error(MPREC_INDEX, "level out of range");
+        if (which != 0 && l == 0) throw Error(MPREC_INDEX, "level 0 has no P/R");
+        Ctx& c = *h->ctx;
+        const AmgLevel& L = *h->amg->lv[l];
+        CsrView m = which == 0 ? L.a : (which == 1 ? L.p.view() : L.r.view());
+        if (rp) MG_CUDA(cudaMemcpyAsync(rp, m.rp, sizeof(int) * (m.n + 1), cudaMemcpyDeviceToHost, c.s));
+        if (ci && m.nnz) MG_CUDA(cudaMemcpyAsync(ci, m.ci, sizeof(int) * m.nnz, cudaMemcpyDeviceToHost, c.s));
+        if (v && m.nnz) MG_CUDA(cudaMemcpyAsync(v, m.v, sizeof(double) * m.nnz, cudaMemcpyDeviceToHost, c.s));
+        c.sync();
+    });
+}
+
+int mprec_gpu_amg_get_cf(mprec_gpu_amg* h, int l, signed char* cf) {
+    return guard([&] {
+        if (l < 0 || l + 1 >= h->amg->n_levels()) throw Error(MPREC_INDEX, "level has no coarsening");
+        Ctx& c = *h->ctx;
+        const AmgLevel& L = *h->amg->lv[l];
+        std::vector<signed char> m = L.cf.to_host(c.s, L.n);
+        for (int i = 0; i < L.n; ++i) cf[i] = m[i] == 1 ? 1 : 0;
+    });
+}
+
+void mprec_gpu_amg_destroy(mprec_gpu_amg* h) {
+    if (!h || !h->own_amg) return;  // views are owned by their system
+    delete h;
+}
+
+// ------------------------------------------------------------------ ILU ---
+int mprec_gpu_ilu_create(const mprec_bsr* a, mprec_gpu_ilu** out) {
+    return guard([&] {
+        if (!a || !out) throw Error(MPREC_DIMENSION, "null argument");
+        auto h = std::make_unique<mprec_gpu_ilu>();
+        load_pattern(h->ctx, h->pat, a->n_cells, a->nb, a->row_ptr, a->col_idx);
+        const size_t nv = std::max<size_t>(size_t(h->pat.nnzb) * a->nb * a->nb, 1);
+        h->vals.upload(a->values, nv, h->ctx.s);
+        h->ilu.lu = view_of(h->pat, a->nb, h->vals.p);
+        h->ilu.pat = &h->pat;
+        h->ilu.factor(h->ctx);
+        h->ctx.sync();
+        *out = h.release();
+    });
+}
+
+int mprec_gpu_ilu_apply(mprec_gpu_ilu* h, const double* r, double* y) {
+    return guard([&] {
+        const int64_t n = int64_t(h->pat.nc) * h->ilu.lu.nb;
+        h->r.upload(r, n, h->ctx.s);
+        h->y.ensure(n);
+        h->ilu.apply(h->ctx, h->r.p, h->y.p);
+        h->y.download(y, n, h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_ilu_get(mprec_gpu_ilu* h, double* lu) {
+    return guard([&] {
+        h->vals.download(lu, size_t(h->pat.nnzb) * h->ilu.lu.nb * h->ilu.lu.nb, h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+void mprec_gpu_ilu_destroy(mprec_gpu_ilu* h) { delete h; }
+
+// ---------------------------------------------------------------- GMRES ---
+int mprec_gpu_gmres(const mprec_bsr* a, const double* b, int prec_kind, void* prec, double tol, int max_iter,
+                    double* x, mprec_solve_result* out, double* history, int history_cap) {
+    return guard([&] {
+        if (!a) throw Error(MPREC_DIMENSION, "null argument");
+        std::unique_ptr<Ctx> own;
+        Ctx* c = nullptr;
+        if (prec_kind == 1)
+            c = static_cast<mprec_gpu_amg*>(prec)->ctx;
+        else if (prec_kind == 2)
+            c = &static_cast<mprec_gpu_ilu*>(prec)->ctx;
+        else if (prec_kind == 0) {
+            own = std::make_unique<Ctx>();
+            c = own.get();
+        } else
+            throw Error(MPREC_CONFIG, "unknown preconditioner kind");
+        Pattern pat;
+        load_pattern(*c, pat, a->n_cells, a->nb, a->row_ptr, a->col_idx);
+        const int64_t n = int64_t(a->n_cells) * a->nb;
+        DBuf<double> vals, bd, xd, tmp;
+        vals.upload(a->values, std::max<size_t>(size_t(pat.nnzb) * a->nb * a->nb, 1), c->s);
+        bd.upload(b, n, c->s);
+        xd.ensure(n);
+        tmp.ensure(n);
+        const BsrView av = view_of(pat, a->nb, vals.p);
+        const DevOp Aop = [&](const double* xx, double* yy) { bsr_spmv(*c, av, xx, yy, nullptr, MPREC_K_SPMV); };
+        DevOp Mop;
+        if (prec_kind == 0)
+            Mop = [&](const double* xx, double* yy) { copy(*c, yy, xx, n); };
+        else if (prec_kind == 1) {
+            auto* ah = static_cast<mprec_gpu_amg*>(prec);
+            if (ah->amg->lv[0]->n != n) throw Error(MPREC_DIMENSION, "preconditioner dimension mismatch");
+            Mop = [&, ah](const double* xx, double* yy) { ah->amg->apply(*c, xx, yy); };
+        } else {
+            auto* ih = static_cast<mprec_gpu_ilu*>(prec);
+            Mop = [&, ih](const double* xx, double* yy) { ih->ilu.apply(*c, xx, yy); };
+        }
+        const double t0 = now_s();
+        Krylov kr;
+        const GmresOut g = gmres_dev(*c, kr, n, Aop, Mop, bd.p, tol, max_iter, xd.p);
+        xd.download(x, n, c->s);
+        c->sync();
+        fill_result(out, g, 1, 0.0, now_s() - t0, history, history_cap);
+    });
+}
+
+// ----------------------------------------------------------- measurement ---
+int mprec_gpu_profile(mprec_gpu_system* h, int enable) {
+    return guard([&] {
+        h->ctx.harvest();
+        h->ctx.profile = enable != 0;
+    });
+}
+
+int mprec_gpu_kernel_stats(mprec_gpu_system* h, int kc, double* ms, int64_t* launches, double* bytes) {
+    return guard([&] {
+        if (kc < 0 || kc >= MPREC_K_COUNT) throw Error(MPREC_INDEX, "kernel class out of range");
+        h->ctx.harvest();
+        if (ms) *ms = h->ctx.stat[kc].ms;
+        if (launches) *launches = h->ctx.stat[kc].launches;
+        if (bytes) *bytes = h->ctx.stat[kc].bytes;
+    });
+}
+
+int mprec_gpu_reset_stats(mprec_gpu_system* h) {
+    return guard([&] { h->ctx.reset_stats(); });
+}
+
+int mprec_gpu_launch_count(mprec_gpu_system* h, int64_t* launches) {
+    return guard([&] { *launches = h->ctx.launches; });
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// common.cuh -- runtime infrastructure of libmprec_gpu.so: errors, device
+// buffers, the per-handle stream context, launch accounting and kernel-class
+// timing.  Every kernel in this library is launched through Ctx so that launch
+// counts and (when profiling) CUDA-event durations are recorded on the stream
+// the kernel actually runs on.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mprec_gpu.h"
+
+namespace mg {
+
+struct Error : std::runtime_error {
+    int code;
+    int payload;
+    Error(int c, const std::string& m, int p = -1) : std::runtime_error(m), code(c), payload(p) {}
+};
+
+#define MG_CUDA(expr)                                                                            \
+    do {                                                                                         \
+        cudaError_t _e = (expr);                                                                 \
+        if (_e != cudaSuccess)                                                                   \
+            throw ::mg::Error(MPREC_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+inline void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(MPREC_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- device buffer ---------------------------------------------------------
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+        o.p = nullptr;
+        o.n = 0;
+    }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) MG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void ensure(size_t count) {
+        if (count > n) alloc(count);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    void upload(const T* h, size_t count, cudaStream_t s) {
+        ensure(count);
+        if (count) MG_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void download(T* h, size_t count, cudaStream_t s) const {
+        if (count) MG_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<T> to_host(cudaStream_t s, size_t count = size_t(-1)) const {
+        if (count == size_t(-1)) count = n;
+        std::vector<T> h(count);
+        download(h.data(), count, s);
+        MG_CUDA(cudaStreamSynchronize(s));
+        return h;
+    }
+};
+
+// ---- per-handle execution context -------------------------------------------
+struct KStat {
+    double ms = 0.0;
+    int64_t launches = 0;
+    double bytes = 0.0;
+};
+
+struct Ctx {
+    cudaStream_t s = nullptr;
+    int sm_count = 148;
+    bool profile = false;
+    int64_t launches = 0;
+    KStat stat[MPREC_K_COUNT];
+    // pending event pairs (class, bytes, start, stop) harvested at sync points
+    struct Pending {
+        int kc;
+        double bytes;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    DBuf<double> red;      // reduction partials
+    DBuf<unsigned> red_ctr;  // last-block counters
+    DBuf<double> scal;     // device scalars (norms, dots)
+    DBuf<int> counters;    // work-distribution counters
+    DBuf<int> err;         // device error slots
+
+    Ctx();
+    ~Ctx();
+    Ctx(const Ctx&) = delete;
+    Ctx& operator=(const Ctx&) = delete;
+
+    cudaEvent_t get_event();
+    // Bracket a launch of kernel class kc with algorithmic byte count `bytes`.
+    struct Scope {
+        Ctx* c;
+        int kc;
+        double bytes;
+        cudaEvent_t a = nullptr;
+        Scope(Ctx* c_, int kc_, double bytes_);
+        ~Scope();
+    };
+    void harvest();  // fold completed event pairs into stat (synchronizes)
+    void sync() {
+        MG_CUDA(cudaStreamSynchronize(s));
+        if (!pending.empty()) harvest();
+    }
+    void reset_stats() {
+        harvest();
+        for (auto& k : stat) k = KStat{};
+        launches = 0;
+    }
+};
+
+constexpr int kRedBlocks = 1184;  // 8 x 148: partials of the deterministic reductions
+
+inline int grid_for(int64_t work, int threads, int cap = 148 * 32) {
+    int64_t g = (work + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return int(g);
+}
+
+}  // namespace mg

@@ -1,0 +1,146 @@
+// mprec.cuh -- internal C++ interface of libmprec_gpu.so (device data
+// structures and kernel launchers).  The C ABI (include/mprec_gpu.h) is
+// implemented on top of this in capi.cu.
+#pragma once
+
+#include <memory>
+
+#include "common.cuh"
+
+namespace mg {
+
+// Sentinel written into the output vectors of the dependency-scheduled sweeps
+// (ILU(0) solves, Gauss-Seidel) before a sweep: a signalling NaN that IEEE
+// arithmetic never produces, so a consumer can poll the value itself.
+constexpr unsigned long long kPending = 0xFFF4DEADBEEFCAFEull;
+
+// ---- views -------------------------------------------------------------------
+struct BsrView {
+    int nc = 0, nb = 0, nnzb = 0;
+    const int* rp = nullptr;
+    const int* ci = nullptr;
+    const int* dpos = nullptr;
+    double* val = nullptr;  // column-major nb x nb blocks
+};
+
+struct CsrView {
+    int n = 0, m = 0, nnz = 0;  // rows, cols, nonzeros
+    const int* rp = nullptr;
+    const int* ci = nullptr;
+    const double* v = nullptr;
+    const int* diag = nullptr;  // position of the diagonal entry per row (square only)
+};
+
+// Block pattern shared by A, Ā and the ILU(0) factors.
+struct Pattern {
+    int nc = 0, nnzb = 0;
+    DBuf<int> rp, ci, dpos;
+    std::vector<int> h_rp, h_ci, h_dpos;
+};
+
+// Owned CSR.
+struct DCsr {
+    int n = 0, m = 0, nnz = 0;
+    DBuf<int> rp, ci, diag;
+    DBuf<double> v;
+    CsrView view() const { return CsrView{n, m, nnz, rp.p, ci.p, v.p, diag.p}; }
+};
+
+// ---- blas.cu -----------------------------------------------------------------
+void fill(Ctx& c, double* x, double val, int64_t n);
+void fill_pending(Ctx& c, double* x, int64_t n);
+void copy(Ctx& c, double* y, const double* x, int64_t n);
+// out_dev <- sum a_i b_i (deterministic fixed-order two-level reduction)
+void dot(Ctx& c, const double* a, const double* b, int64_t n, double* out_dev);
+// out_dev <- ||a||_2
+void nrm2(Ctx& c, const double* a, int64_t n, double* out_dev);
+// MGS step of gmres.cpp:39-50, fused:
+//   if (gate == nullptr || *gate) { if (vprev) w -= (*hprev_scale) * vprev;
+//                                   if (vcur) *hout = vcur . w (+= if accumulate) }
+// hprev is read from device memory (the previous dot), so no host sync.
+void mgs_step(Ctx& c, double* w, const double* vprev, const double* hprev, const double* vcur,
+              int64_t n, double* hout, bool accumulate, double* hsum, const int* gate);
+// gate_dev <- (||w|| < 0.7 * pre_norm) evaluated on device scalars
+void set_reorth_gate(Ctx& c, const double* wnorm, const double* prenorm, int* gate);
+// y = x / alpha (host scalar)
+void div_scalar(Ctx& c, double* y, const double* x, double alpha, int64_t n);
+// z = sum_i y[i] * V[i] (device pointer table, host-provided coefficients)
+void multi_axpy(Ctx& c, double* z, const double* const* vtab_dev, const double* y_dev, int k, int64_t n);
+// out = b - ax ; optional
+void sub(Ctx& c, double* out, const double* b, const double* ax, int64_t n);
+// out[c] = x[c*stride + f]
+void gather_stride(Ctx& c, double* out, const double* x, int nc, int stride, int f);
+// y[i] = w[i] + s[i] where s is the scatter of the stage solutions (xs on field fx,
+// vs on field fv; either may be null)
+void stage_combine(Ctx& c, double* y, const double* w, const double* xs, int fx, const double* vs, int fv,
+                   int nc, int nb);
+
+// ---- bsr.cu ------------------------------------------------------------------
+// y = A x  or  y = b - A x  (b != nullptr); flat (scalar-CSR) semantics
+void bsr_spmv(Ctx& c, const BsrView& a, const double* x, double* y, const double* b, int kclass);
+// z = r - A[:, field f] xs  (xs: one value per cell = the stage solution scattered
+// to field f); optionally gather zsub[c] = z[c*nb + g]
+void bsr_col_update(Ctx& c, const BsrView& a, int f, const double* xs, const double* r, double* z,
+                    double* zsub, int g);
+
+// ---- scaling.cu --------------------------------------------------------------
+// In-place left scaling of Ā and b̄ (scaling.cpp:73-147); throws mg::Error
+// (SINGULAR_BLOCK with the reference's tag and cell) after synchronising.
+void left_scale(Ctx& c, const BsrView& abar, double* bbar, int method);
+// vals[k] = A_k(f, f)  (extract_submatrix on a single field, pattern = block pattern)
+void extract_field(Ctx& c, const BsrView& a, int f, double* vals);
+
+// ---- ilu.cu ------------------------------------------------------------------
+struct Ilu {
+    BsrView lu;           // values owned elsewhere (or by `own`)
+    DBuf<double> own;     // factor storage when the Ilu owns it
+    DBuf<double> ybuf;    // forward-sweep output
+    DBuf<int> flags;      // factorisation ready flags
+    const Pattern* pat = nullptr;
+    int n = 0;
+    // factor in place (values of lu are overwritten by L\U); throws ZERO_PIVOT/SETUP
+    void factor(Ctx& c);
+    // y = U^-1 L^-1 r  (ilu0.cpp:41-59); y must not alias r
+    void apply(Ctx& c, const double* r, double* y);
+};
+
+// ---- amg.cu ------------------------------------------------------------------
+struct AmgParams {
+    double theta = 0.25;
+    int max_coarse = 1000;
+    int max_levels = 25;
+};
+
+struct AmgLevel {
+    int n = 0;
+    CsrView a;            // level operator (level 0 may be a non-owning view)
+    DCsr a_own, p, r;     // p/r: interpolation into the finer level (levels >= 1)
+    DBuf<signed char> cf; // C/F splitting of this level (levels < last)
+    DBuf<double> x, b, t, xf, xb;  // work vectors
+};
+
+struct Amg {
+    AmgParams prm;
+    std::vector<std::unique_ptr<AmgLevel>> lv;
+    DBuf<double> coarse_inv;  // row-major inverse of the coarsest operator
+    DBuf<double> coarse_lu;   // LU factors (diagnostic / parity)
+    int nco = 0;
+    DCsr a0_copy;             // when the caller's matrix must be owned
+    // AMGHierarchy::setup (amg.cpp:188-214). a0 must stay alive.
+    void setup(Ctx& c, const CsrView& a0, const AmgParams& p);
+    // AMGHierarchy::apply (amg.cpp:233-238): x = V(1,1)-cycle(r), zero initial guess.
+    void apply(Ctx& c, const double* r, double* x);
+    int n_levels() const { return int(lv.size()); }
+   private:
+    void cycle(Ctx& c, int l, const double* r, double* x);
+};
+
+// csr.cu helpers
+void csr_spmv(Ctx& c, const CsrView& a, const double* x, double* y, const double* b, bool add_to_y,
+              int kclass);
+// forward (dir=+1) / backward (dir=-1) Gauss-Seidel sweep, dependency scheduled
+void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, double* xnew, int dir,
+              bool xold_zero);
+void dense_gemv(Ctx& c, const double* m_rowmajor, int n, const double* x, double* y);
+
+}  // namespace mg
