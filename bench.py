@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the GMRES / CPTR3 solve path on B200 (BASELINE.json metric:
+"GMRES solve time & iters/sec; SpMV/V-cycle HBM GB/s").
+
+Workload (default): BASELINE.json config 5 -- 2000x2000 grid, 4M cells, nb=8
+(32M unknowns, 19.99M 8x8 fp64 blocks = 10.24 GB of matrix), reaction band,
+log-normal permeability, cptr3-amg, tol 1e-8, max_iter 500, synthetic data
+from the seeded generator.  One step = one complete GMRES solve
+(solve_system after setup: up to 3 tolerance-tightening attempts, true
+residual on the original A) with A, Ā, the preconditioner and b already
+resident in HBM.  value = GMRES iterations (all attempts) / second, device
+time measured with CUDA events on the library's stream, max over ranks.
+e2e = the same metric through the C ABI `mprec_gpu_solve_system` from HOST
+buffers (H2D of A and b, setup, solve, D2H of x inside the timed region).
+
+--impl reference times the reference's CPU path (the oracle restatement:
+the reference itself cannot be built here) on the host cores:
+setup once (untimed), then every step = a bounded sample of 2 GMRES
+iterations of the same system.
+
+Multi-GPU: replicas only: every rank solves its own copy of the
+system, no collective on the data path; rank 0 prints the JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KCLASS = ["spmv", "spmv_col", "ilu_fwd", "ilu_bwd", "gs", "csr", "coarse", "mgs", "blas1"]
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=5)
+    p.add_argument("--method", default="cptr3-amg")
+    p.add_argument("--tol", type=float, default=1e-8)
+    p.add_argument("--max-iter", type=int, default=500)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--ref-sample-iters", type=int, default=2)
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def load_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload(cfg, method):
+    from paper_1912_04385_b200 import gen
+    s = gen.config_spec(cfg)
+    nc = s.nx * s.ny
+    return {"workload": f"BASELINE config {cfg}: {s.nx}x{s.ny} grid, nb={s.nb}, {method}",
+            "cells": nc, "unknowns": nc * s.nb, "nnzb": int(gen._load().mprec_gen_nnzb(s.nx, s.ny)),
+            "kappa": s.kappa, "perm_sigma": s.perm_sigma, "reaction_band": bool(s.band), "seed": int(s.seed),
+            "method": method, "tol": None, "max_iter": None}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(5)
+            except Exception:
+                self.p.kill()
+        self.f.flush()
+        rows = []
+        try:
+            with open(self.f.name) as fh:
+                for line in fh:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 8:
+                        rows.append(parts)
+        finally:
+            os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                util = float(r[7])
+                if util > 0:
+                    sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for k, name in enumerate(names):
+                if r[3 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------- reference --
+def run_reference_sample(cfg, method, sample_iters, steps, warmup, out=None):
+    """Oracle (the reference's CPU path restated) on the host: setup once,
+    then `steps` timed samples of `sample_iters` GMRES iterations each."""
+    import oracle
+    from paper_1912_04385_b200 import gen
+    o = oracle.api()
+    a, b, _ = gen.generate(cfg)
+    t0 = time.perf_counter()
+    s = o.system(a).setup(method, b)
+    setup_s = time.perf_counter() - t0
+    times, iters = [], []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        r = s.solve(1e-8, sample_iters)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+            iters.append(r.total_iterations)
+    res = {"setup_s": setup_s, "times": times, "iters": iters,
+           "value": sum(iters) / sum(times) if times else None}
+    if out is not None:
+        out.update(res)
+    return res
+
+
+def reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    w = workload(args.config, args.method)
+    w["tol"], w["max_iter"] = args.tol, args.max_iter
+    steps, warmup = max(args.steps, 1), max(args.warmup, 0)
+    # each step is already a bounded sample; cap the number of samples so the
+    # whole run stays within a few minutes at config 5
+    warm = min(warmup, 1)
+    st = min(steps, 5)
+    r = run_reference_sample(args.config, args.method, args.ref_sample_iters, st, warm)
+    v = r["value"]
+    ms = 1e3 * sum(r["times"]) / len(r["times"])
+    sample = (f"{args.ref_sample_iters} preconditioned GMRES iterations of the full config-{args.config} system per step "
+              f"({st} timed steps after {warm} warm-up; setup {r['setup_s']:.1f}s untimed)")
+    line = {"metric": "gmres_iters_per_s", "value": v, "unit": "iters/s", "n_gpus": world, "steps": st,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded BASELINE generator)", "config": w, "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference = oracle/ C++ restatement of proj/src (reference not buildable: Eigen3 absent)"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- ours --
+def ours(args):
+    import ctypes as C
+
+    import torch
+
+    from paper_1912_04385_b200 import gen
+    from paper_1912_04385_b200.api import gpu, _Result, _ptr
+
+    rank, local, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    api = gpu()
+
+    cpu_res = {}
+    cpu_thread = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # bounded CPU sample of the same workload on the host cores, concurrently
+        cpu_thread = threading.Thread(target=run_reference_sample,
+                                      args=(args.config, args.method, args.ref_sample_iters, 1, 0, cpu_res),
+                                      daemon=True)
+        cpu_thread.start()
+
+    t_gen = time.perf_counter()
+    a, b, xs = gen.generate(args.config)
+    t_gen = time.perf_counter() - t_gen
+    s = api.system(a).setup(args.method, b)
+    stream = C.c_void_p()
+    api.call("stream", s.h, C.byref(stream))
+    ext = torch.cuda.ExternalStream(stream.value, device=dev)
+    res = _Result()
+
+    def solve_once():
+        api.call("solve_dev", s.h, args.tol, args.max_iter, None, C.byref(res))
+        return res.total_iterations, res.converged, res.final_true_residual, res.attempts, res.iterations
+
+    for _ in range(args.warmup):
+        solve_once()
+    # timed region: barrier + sync on both sides, CUDA events on the library stream
+    api.call("reset_stats", s.h)
+    api.call("profile", s.h, 1)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(ext)
+    tot_it, info = 0, None
+    for _ in range(args.steps):
+        it, conv, tr, att, last = solve_once()
+        tot_it += it
+        info = dict(converged=bool(conv), final_true_residual=tr, attempts=att, iterations_last_attempt=last,
+                    iterations_total=it)
+    ev1.record(ext)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = C.c_int64()
+    api.call("launch_count", s.h, C.byref(launches))
+    stats = {}
+    for k, name in enumerate(KCLASS):
+        t, n, by = C.c_double(), C.c_int64(), C.c_double()
+        api.call("kernel_stats", s.h, k, C.byref(t), C.byref(n), C.byref(by))
+        stats[name] = {"ms": t.value, "launches": n.value, "bytes": by.value}
+    api.call("profile", s.h, 0)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = world * tot_it / (ms / 1e3)
+
+    # e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        x = np.zeros(a.dim)
+        r2 = _Result()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        api.call("solve_system", C.byref(a._c), _ptr(b), s.method, args.tol, args.max_iter, _ptr(x), C.byref(r2))
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([el], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            el = float(tt.item())
+        h2d = a.row_ptr.nbytes + a.col_idx.nbytes + a.values.nbytes + b.nbytes
+        e2e = {"value": world * r2.total_iterations / el, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(x.nbytes), "seconds": el, "setup_s": r2.setup_s,
+               "iterations": r2.total_iterations, "x_err_vs_xstar": float(np.linalg.norm(x - xs) / np.linalg.norm(xs))}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return 0
+
+    # roofline of the dominant kernel class (largest share of the timed region)
+    peak, peak_kind = load_peak()
+    dom = max(stats, key=lambda k: stats[k]["ms"])
+    d = stats[dom]
+    avg_ms = d["ms"] / max(d["launches"], 1)
+    avg_bytes = d["bytes"] / max(d["launches"], 1)
+    achieved = avg_bytes / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    spmv = stats["spmv"]
+    spmv_gbs = (spmv["bytes"] / spmv["launches"]) / (spmv["ms"] / spmv["launches"] / 1e3) / 1e9 if spmv["ms"] else None
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+            "per_class": {k: {"share": v["ms"] / max(ms, 1e-9), "launches": v["launches"],
+                              "GBps": (v["bytes"] / v["ms"] * 1e3 / 1e9) if v["ms"] > 0 else None}
+                          for k, v in stats.items()},
+            "spmv_GBps": spmv_gbs, "spmv_frac": (spmv_gbs / peak) if spmv_gbs else None}
+    if cpu_thread is not None:
+        cpu_thread.join()
+    cpu = None
+    if cpu_res.get("value"):
+        cpu = {"value": cpu_res["value"], "unit": "iters/s", "cores": 1, "kind": "port",
+               "sample": f"{args.ref_sample_iters} preconditioned GMRES iterations of the full config-{args.config} "
+                         f"system on the oracle (setup {cpu_res['setup_s']:.1f}s untimed)"}
+    w = workload(args.config, args.method)
+    w["tol"], w["max_iter"] = args.tol, args.max_iter
+    w["l2"] = "inputs larger than L2 (10.24 GB matrix per operator pass)" if args.config == 5 else "see unknowns"
+    w["parallelism"] = f"replicas x{world} (no data-path collective)"
+    w["solve"] = info
+    line = {"metric": "gmres_iters_per_s", "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE generator)", "config": w,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches.value),
+            "clocks": clk, "generate_s": t_gen}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

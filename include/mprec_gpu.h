@@ -83,6 +83,7 @@ typedef struct mprec_solve_result {
     double final_true_residual; /* ||b - A x|| / ||b|| on the ORIGINAL system */
     double setup_s;             /* left_scale + build_preconditioner */
     double solve_s;             /* all GMRES attempts */
+    int total_iterations;       /* summed over all attempts */
 } mprec_solve_result;
 
 typedef struct mprec_gpu_system mprec_gpu_system; /* opaque */
@@ -188,6 +189,9 @@ typedef enum mprec_kernel_class {
 } mprec_kernel_class;
 
 int mprec_gpu_profile(mprec_gpu_system* h, int enable);
+/* The handle's CUDA stream (cudaStream_t) -- every kernel of the handle runs
+ * on it, so callers can bracket work with their own CUDA events. */
+int mprec_gpu_stream(mprec_gpu_system* h, void** stream);
 /* accumulated since the last reset: total device ms, launches, algorithmic bytes */
 int mprec_gpu_kernel_stats(mprec_gpu_system* h, int kclass, double* ms, int64_t* launches,
                            double* bytes);

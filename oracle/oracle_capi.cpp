@@ -147,10 +147,11 @@ int orc_solve(orc_system* h, double tol, int max_iter, double* x, mprec_solve_re
         const Op abar = [h](const Vec& v) { return h->sc.a_bar.apply_flat(v); };
         const Op mop = [h](const Vec& v) { return h->prec.apply(v); };
         SolveResult res;
-        int attempts = 0;
+        int attempts = 0, total = 0;
         for (int attempt = 0; attempt < 3; ++attempt) {
             ++attempts;
             res = gmres(h->a.dim(), abar, h->sc.b_bar, mop, opts);
+            total += res.iterations;
             res.final_true_residual = residual_check(orig, h->b, res.x);
             if (!res.converged || res.final_true_residual <= tol) break;
             opts.tol *= 0.5 * tol / res.final_true_residual;
@@ -161,6 +162,7 @@ int orc_solve(orc_system* h, double tol, int max_iter, double* x, mprec_solve_re
         out->converged = res.converged;
         out->breakdown = res.breakdown;
         out->attempts = attempts;
+        out->total_iterations = total;
         out->final_true_residual = res.final_true_residual;
         out->setup_s = h->setup_s;
         out->solve_s = now_s() - t0;
@@ -310,6 +312,7 @@ int orc_gmres(const mprec_bsr* a, const double* b, int prec_kind, void* prec, do
         out->converged = res.converged;
         out->breakdown = res.breakdown;
         out->attempts = 1;
+        out->total_iterations = res.iterations;
         out->final_true_residual = res.final_true_residual;
         out->setup_s = 0.0;
         out->solve_s = now_s() - t0;

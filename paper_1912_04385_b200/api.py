@@ -108,7 +108,7 @@ class _Csr(C.Structure):
 class _Result(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int), ("attempts", C.c_int),
                 ("history_len", C.c_int), ("final_true_residual", C.c_double), ("setup_s", C.c_double),
-                ("solve_s", C.c_double)]
+                ("solve_s", C.c_double), ("total_iterations", C.c_int)]
 
 
 @dataclass
@@ -123,6 +123,7 @@ class SolveResult:
     final_true_residual: float
     setup_time_s: float
     wall_time_s: float
+    total_iterations: int = 0
 
 
 def _f64(a) -> np.ndarray:
@@ -264,6 +265,7 @@ class Api:
             "kernel_stats": (C.c_int, [vp, C.c_int, dp, i64p, dp]),
             "reset_stats": (C.c_int, [vp]),
             "launch_count": (C.c_int, [vp, i64p]),
+            "stream": (C.c_int, [vp, C.POINTER(vp)]),
         }
         self.fn = {}
         for name, (res, args) in list(sig.items()) + list(optional.items()):
@@ -325,7 +327,7 @@ def _result(x, res: _Result, hist) -> SolveResult:
                        breakdown=bool(res.breakdown), attempts=res.attempts,
                        residual_history=np.array(hist[:res.history_len]),
                        final_true_residual=res.final_true_residual, setup_time_s=res.setup_s,
-                       wall_time_s=res.solve_s)
+                       wall_time_s=res.solve_s, total_iterations=res.total_iterations)
 
 
 class System:

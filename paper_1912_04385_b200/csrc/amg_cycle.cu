@@ -14,46 +14,61 @@
 namespace mg {
 namespace {
 
-__device__ __forceinline__ double ld_poll(const double* p) {
-    unsigned long long v;
-    do {
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    } while (v == kPending);
-    return __longlong_as_double((long long)v);
-}
 __device__ __forceinline__ void st_pub(double* p, double v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
 }
 
 constexpr int kGsWarps = 8;
 
+__device__ __forceinline__ unsigned long long ld_relaxed(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Warp per row.  The wait is warp-CONVERGENT (every lane stays in one
+// __any_sync loop): a divergent spin under independent thread scheduling
+// serialises the warp's paths and costs ~100x the hop latency.
 template <int DIR>
 __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp, const int* __restrict__ ci,
                                                       const double* __restrict__ v, const int* __restrict__ diag,
                                                       const double* __restrict__ b, const double* __restrict__ xold,
-                                                      double* xnew, int n, int* counter) {
+                                                      double* xnew, int n, const int* __restrict__ order,
+                                                      int* counter) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         int t = 0;
         if (lane == 0) t = atomicAdd(counter, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= n) return;
-        const int i = DIR > 0 ? t : n - 1 - t;
+        const int i = __ldg(order + t);
+        const int k0 = __ldg(rp + i), k1 = __ldg(rp + i + 1);
+        // independent of the dependency chain: issue before waiting
+        const double bi = __ldg(b + i), dii = __ldg(v + __ldg(diag + i));
         double acc = 0.0;
-        for (int k = rp[i] + lane; k < rp[i + 1]; k += 32) {
-            const int j = __ldg(ci + k);
-            if (j == i) continue;
-            const double a = __ldg(v + k);
-            double xj;
-            if (DIR > 0 ? (j < i) : (j > i))
-                xj = ld_poll(xnew + j);
-            else
-                xj = xold ? __ldg(xold + j) : 0.0;
+        for (int base = k0; base < k1; base += 32) {
+            const int k = base + lane;
+            const bool valid = k < k1;
+            const int j = valid ? __ldg(ci + k) : i;
+            const bool off = valid && j != i;
+            const double a = off ? __ldg(v + k) : 0.0;
+            const bool dep = off && (DIR > 0 ? (j < i) : (j > i));
+            double xj = 0.0;
+            if (off && !dep && xold) xj = __ldg(xold + j);
+            unsigned long long raw = 0;
+            bool pend = dep;
+            while (__any_sync(0xffffffffu, pend)) {
+                if (pend) {
+                    raw = ld_relaxed(xnew + j);
+                    pend = raw == kPending;
+                }
+            }
+            if (dep) xj = __longlong_as_double((long long)raw);
             acc += a * xj;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) st_pub(xnew + i, (b[i] - acc) / v[diag[i]]);
+        if (lane == 0) st_pub(xnew + i, (bi - acc) / dii);
     }
 }
 
@@ -88,7 +103,8 @@ __global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ m, int 
 
 }  // namespace
 
-void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, double* xnew, int dir, bool xold_zero) {
+void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, double* xnew, int dir, bool xold_zero,
+              const int* order) {
     const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 4.0 * a.n + 24.0 * a.n;
     Ctx::Scope sc(&c, MPREC_K_GS, bytes);
     int* ctr = c.counters.p + 4;
@@ -96,10 +112,10 @@ void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, dou
     const int blocks = std::max(1, std::min((a.n + kGsWarps - 1) / kGsWarps, c.sm_count * 8));
     if (dir > 0)
         k_gs<1><<<blocks, kGsWarps * 32, 0, c.s>>>(a.rp, a.ci, a.v, a.diag, b, xold_zero ? nullptr : xold, xnew, a.n,
-                                                   ctr);
+                                                   order, ctr);
     else
         k_gs<-1><<<blocks, kGsWarps * 32, 0, c.s>>>(a.rp, a.ci, a.v, a.diag, b, xold_zero ? nullptr : xold, xnew,
-                                                    a.n, ctr);
+                                                    a.n, order, ctr);
     check_launch("gs_sweep");
 }
 
@@ -132,9 +148,9 @@ void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
     const int64_t n = L.n;
     // x = 0; sym GS
     fill_pending(c, L.xf.p, n);
-    gs_sweep(c, L.a, r, nullptr, L.xf.p, +1, true);
+    gs_sweep(c, L.a, r, nullptr, L.xf.p, +1, true, L.ofwd);
     fill_pending(c, x, n);
-    gs_sweep(c, L.a, r, L.xf.p, x, -1, false);
+    gs_sweep(c, L.a, r, L.xf.p, x, -1, false, L.obwd);
     // rc = R (r - A x)
     csr_spmv(c, L.a, x, L.t.p, r, false, MPREC_K_CSR);
     csr_spmv(c, N.r.view(), L.t.p, N.b.p, nullptr, false, MPREC_K_CSR);
@@ -143,9 +159,9 @@ void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
     csr_spmv(c, N.p.view(), N.x.p, x, nullptr, true, MPREC_K_CSR);
     // post sym GS
     fill_pending(c, L.xf.p, n);
-    gs_sweep(c, L.a, r, x, L.xf.p, +1, false);
+    gs_sweep(c, L.a, r, x, L.xf.p, +1, false, L.ofwd);
     fill_pending(c, x, n);
-    gs_sweep(c, L.a, r, L.xf.p, x, -1, false);
+    gs_sweep(c, L.a, r, L.xf.p, x, -1, false, L.obwd);
 }
 
 // amg.cpp:233-238

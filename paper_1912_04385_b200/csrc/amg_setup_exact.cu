@@ -740,6 +740,7 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
     DBuf<int> scnt(n), stcnt(n), srp(n + 1), strp(n + 1), stfill(n);
     MG_CUDA(cudaMemsetAsync(stcnt.p, 0, sizeof(int) * n, c.s));
     MG_CUDA(cudaMemsetAsync(stfill.p, 0, sizeof(int) * n, c.s));
+    Trace tr_s(&c, "amg strength");
     k_strength_count<<<nblk(n), 256, 0, c.s>>>(a.rp, a.ci, a.v, n, theta, mrow.p, scnt.p, stcnt.p);
     const int ns = scan(c, s, scnt.p, srp.p, n);
     scan(c, s, stcnt.p, strp.p, n);
@@ -778,12 +779,14 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
     k_bq_summary<<<nblk((int64_t)q.n1 * nbuckets), 256, 0, c.s>>>(l0.p, l1.p, q.n0, q.n1, nbuckets);
     k_bq_summary<<<nblk((int64_t)q.n2 * nbuckets), 256, 0, c.s>>>(l1.p, l2.p, q.n1, q.n2, nbuckets);
     {
+        Trace tr(&c, "amg rs first pass");
         Ctx::Scope sc(&c, MPREC_K_BLAS1, 0.0);
         k_rs_select<<<1, 32, 0, c.s>>>(srp.p, sci.p, strp.p, stci.p, mark, lam.p, q, nbuckets, inc.p, jlist.p,
                                        klist.p);
         check_launch("rs first pass");
     }
     // ---- second pass
+    Trace tr2(&c, "amg rs passes 2+3");
     DBuf<int> flag(n), fpos(n + 1), list(n);
     k_rs2_cand<<<nblk(n), 256, 0, c.s>>>(srp.p, sci.p, mark, n, flag.p);
     int ncand = scan(c, s, flag.p, fpos.p, n);
@@ -801,6 +804,7 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
         check_launch("rs third pass");
     }
     // ---- coarse ids + direct interpolation
+    Trace tr3(&c, "amg interpolation");
     DBuf<int> isc(n), cpos(n + 1), pcnt(n);
     k_is_c<<<nblk(n), 256, 0, c.s>>>(mark, n, isc.p);
     const int nc = scan(c, s, isc.p, cpos.p, n);
@@ -848,7 +852,7 @@ static void coarse_factor(Ctx& c, const CsrView& a, DBuf<double>& lu, DBuf<doubl
 }
 
 // AMGHierarchy::setup (amg.cpp:188-214)
-void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p) {
+void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
     prm = p;
     lv.clear();
     Scratch s;
@@ -870,6 +874,7 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p) {
         }
         if (nc > int(0.95 * f.n))
             throw Error(MPREC_SETUP, "AMG coarsening stagnated at size " + std::to_string(f.n));
+        Trace tr(&c, "amg transpose+galerkin");
         transpose(c, s, nl->p, nl->r);
         DCsr ap;
         spgemm(c, s, f.a, nl->p.view(), ap);
@@ -881,7 +886,25 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p) {
         lv.push_back(std::move(nl));
     }
     nco = lv.back()->n;
+    Trace trc(&c, "amg coarse dense LU+inv");
     coarse_factor(c, lv.back()->a, coarse_lu, coarse_inv);
+    {
+        Trace tr(&c, "amg sweep schedules");
+        for (size_t li = 0; li < lv.size(); ++li) {
+            AmgLevel& l = *lv[li];
+            if (li + 1 == lv.size()) break;  // the coarsest level is solved densely
+            if (li == 0 && pat) {
+                pat->ensure_sched(c);
+                l.ofwd = pat->fwd.order.p;
+                l.obwd = pat->bwd.order.p;
+            } else {
+                build_sched(c, l.n, l.a.rp, l.a.ci, +1, l.own_fwd);
+                build_sched(c, l.n, l.a.rp, l.a.ci, -1, l.own_bwd);
+                l.ofwd = l.own_fwd.order.p;
+                l.obwd = l.own_bwd.order.p;
+            }
+        }
+    }
     for (auto& l : lv) {
         l->x.ensure(std::max(l->n, 1));
         l->b.ensure(std::max(l->n, 1));

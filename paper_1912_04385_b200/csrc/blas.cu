@@ -6,6 +6,9 @@
 // block reduces a fixed grid-stride slice through a fixed shared-memory tree,
 // and the last block to finish sums the per-block partials in a fixed order.
 // Repeated solves are therefore bitwise identical (test_krylov.cpp:92-100).
+#include <chrono>
+#include <cstdlib>
+
 #include "mprec.cuh"
 
 namespace mg {
@@ -78,6 +81,32 @@ void Ctx::harvest() {
         event_pool.push_back(p.b);
     }
     pending.clear();
+}
+
+bool trace_on() {
+    static const bool on = [] {
+        const char* e = getenv("MPREC_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+static double wall() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+Trace::Trace(Ctx* c_, const char* w) : what(w), c(c_), t0(0) {
+    if (trace_on()) {
+        c->sync();
+        t0 = wall();
+    }
+}
+
+Trace::~Trace() {
+    if (trace_on()) {
+        cudaStreamSynchronize(c->s);
+        fprintf(stderr, "[mprec] %-28s %9.3f ms\n", what, 1e3 * (wall() - t0));
+    }
 }
 
 // ================================================================== kernels ==

@@ -232,8 +232,9 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
 }
 
 void fill_result(mprec_solve_result* r, const GmresOut& g, int attempts, double setup_s, double solve_s,
-                 double* history, int cap) {
+                 double* history, int cap, int total_iterations = -1) {
     if (!r) return;
+    r->total_iterations = total_iterations < 0 ? g.iterations : total_iterations;
     r->iterations = g.iterations;
     r->converged = g.converged;
     r->breakdown = g.breakdown;
@@ -249,6 +250,10 @@ void fill_result(mprec_solve_result* r, const GmresOut& g, int attempts, double 
 }
 
 }  // namespace
+
+namespace mg {
+void ilu_timeline(Ctx& c, Ilu& ilu, const double* r, double* y, long long* ts_dev, int blocks);
+}
 
 // ============================================================ AMG handle ==
 struct mprec_gpu_amg {
@@ -341,6 +346,7 @@ struct mprec_gpu_system {
         stage_combine(c, yout, w.p, xT.p, f, nullptr, 0, nc, nb);
     }
 
+    int total_iterations = 0;
     GmresOut solve_attempts(double tol, int max_iter, double* xdev, int* attempts) {
         Ctx& c = ctx;
         const DevOp Aop = [this](const double* xx, double* yy) { bsr_spmv(ctx, Abar(), xx, yy, nullptr, MPREC_K_SPMV); };
@@ -352,9 +358,11 @@ struct mprec_gpu_system {
         double opt_tol = tol;
         GmresOut res;
         *attempts = 0;
+        total_iterations = 0;
         for (int attempt = 0; attempt < 3; ++attempt) {
             ++*attempts;
             res = gmres_dev(c, kr, n, Aop, Mop, bbar.p, opt_tol, max_iter, xdev);
+            total_iterations += res.iterations;
             // residual_check on the ORIGINAL system (gmres.cpp:108-112)
             bsr_spmv(c, A(), xdev, kr.t.p, bn == 0.0 ? nullptr : b.p, MPREC_K_SPMV);
             nrm2(c, kr.t.p, n, c.scal.p + 9);
@@ -421,7 +429,10 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
         h->abar_val.ensure(nv);
         MG_CUDA(cudaMemcpyAsync(h->abar_val.p, h->a_val.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.s));
         // left_scale (scaling.cpp:149-158)
-        left_scale(c, h->Abar(), h->bbar.p, method);
+        {
+            Trace tr(&c, "left_scale");
+            left_scale(c, h->Abar(), h->bbar.p, method);
+        }
         // build_preconditioner (stages.cpp:129-138)
         AmgParams prm;
         if (amg) {
@@ -438,21 +449,26 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
             extract_field(c, h->Abar(), h->T(), h->fT.p);
             CsrView a0{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fT.p, h->pat.dpos.p};
             h->amgT = std::make_unique<Amg>();
-            h->amgT->setup(c, a0, prm);
+            Trace tr(&c, "AMG(C_TT) setup total");
+            h->amgT->setup(c, a0, prm, &h->pat);
         }
         if (method != MPREC_METHOD_ILU0) {
             h->fP.ensure(h->pat.nnzb);
             extract_field(c, h->Abar(), h->P(), h->fP.p);
             CsrView a0{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fP.p, h->pat.dpos.p};
             h->amgP = std::make_unique<Amg>();
-            h->amgP->setup(c, a0, prm);
+            Trace tr(&c, "AMG(B_PP) setup total");
+            h->amgP->setup(c, a0, prm, &h->pat);
         }
         // ILU(0) of Ā
         h->lu_val.ensure(nv);
         MG_CUDA(cudaMemcpyAsync(h->lu_val.p, h->abar_val.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.s));
         h->ilu.lu = view_of(h->pat, h->nb, h->lu_val.p);
         h->ilu.pat = &h->pat;
-        h->ilu.factor(c);
+        {
+            Trace tr(&c, "ILU(0) factor");
+            h->ilu.factor(c);
+        }
         for (DBuf<double>* v : {&h->gT, &h->xT, &h->gP, &h->vP}) v->ensure(nc);
         for (DBuf<double>* v : {&h->z, &h->u, &h->w, &h->x, &h->r, &h->y}) v->ensure(n);
         c.sync();
@@ -503,7 +519,7 @@ int mprec_gpu_solve_dev(mprec_gpu_system* h, double tol, int max_iter, double* x
         double* xd = x_dev ? x_dev : h->x.p;
         const GmresOut g = h->solve_attempts(tol, max_iter, xd, &attempts);
         h->ctx.sync();
-        fill_result(out, g, attempts, h->setup_s, now_s() - t0, nullptr, 0);
+        fill_result(out, g, attempts, h->setup_s, now_s() - t0, nullptr, 0, h->total_iterations);
     });
 }
 
@@ -516,7 +532,7 @@ int mprec_gpu_solve(mprec_gpu_system* h, double tol, int max_iter, double* x, mp
         const GmresOut g = h->solve_attempts(tol, max_iter, h->x.p, &attempts);
         h->x.download(x, h->n, h->ctx.s);
         h->ctx.sync();
-        fill_result(out, g, attempts, h->setup_s, now_s() - t0, history, history_cap);
+        fill_result(out, g, attempts, h->setup_s, now_s() - t0, history, history_cap, h->total_iterations);
     });
 }
 
@@ -766,6 +782,26 @@ int mprec_gpu_profile(mprec_gpu_system* h, int enable) {
         h->ctx.harvest();
         h->ctx.profile = enable != 0;
     });
+}
+
+// Diagnostics (not in the public header): timeline of one forward ILU sweep.
+int mprec_gpu_debug_ilu_timeline(mprec_gpu_system* h, int blocks, long long* ts, int* order, int* nlev) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        DBuf<long long> t(2 * h->pat.nc);
+        fill(h->ctx, h->r.p, 1.0, h->n);
+        const double t0 = now_s();
+        ilu_timeline(h->ctx, h->ilu, h->r.p, h->y.p, t.p, blocks);
+        fprintf(stderr, "ilu fwd sweep wall %.3f ms\n", 1e3 * (now_s() - t0));
+        t.download(ts, 2 * h->pat.nc, h->ctx.s);
+        h->pat.fwd.order.download(order, h->pat.nc, h->ctx.s);
+        *nlev = h->pat.fwd.nlev;
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_stream(mprec_gpu_system* h, void** stream) {
+    return guard([&] { *stream = (void*)h->ctx.s; });
 }
 
 int mprec_gpu_kernel_stats(mprec_gpu_system* h, int kc, double* ms, int64_t* launches, double* bytes) {

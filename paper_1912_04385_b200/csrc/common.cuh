@@ -144,6 +144,16 @@ struct Ctx {
     }
 };
 
+// MPREC_TRACE=1: setup phase timings on stderr (synchronising; diagnostics only)
+bool trace_on();
+struct Trace {
+    const char* what;
+    Ctx* c;
+    double t0;
+    Trace(Ctx* c_, const char* w);
+    ~Trace();
+};
+
 constexpr int kRedBlocks = 1184;  // 8 x 148: partials of the deterministic reductions
 
 inline int grid_for(int64_t work, int threads, int cap = 148 * 32) {

@@ -32,7 +32,8 @@ constexpr int kMaxNb = 16;
 
 __global__ void __launch_bounds__(kWarps * 32) k_ilu_factor(const int* __restrict__ rp, const int* __restrict__ ci,
                                                             const int* __restrict__ dpos, double* val, int nc, int nb,
-                                                            int* flags, int epoch, int* counter, int* zero_flag) {
+                                                            int* flags, int epoch, const int* __restrict__ order,
+                                                            int* counter, int* zero_flag) {
     __shared__ double fac_sh[kWarps][kMaxNb];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double* fac = fac_sh[wid];
@@ -42,6 +43,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu_factor(const int* __restric
         if (lane == 0) I = atomicAdd(counter, 1);
         I = __shfl_sync(0xffffffffu, I, 0);
         if (I >= nc) return;
+        I = order[I];
         const int k0 = rp[I], k1 = rp[I + 1], d = dpos[I];
         // ---- phase 1: lower blocks (I,K), K ascending
         for (int k = k0; k < d; ++k) {
@@ -164,8 +166,9 @@ static int first_zero_pivot(const std::vector<double>& diag, const Pattern* pat,
     return best_row;
 }
 
-void ilu_factor_run(Ctx& c, const BsrView& lu, DBuf<int>& flags, const Pattern* pat) {
+void ilu_factor_run(Ctx& c, const BsrView& lu, DBuf<int>& flags, Pattern* pat) {
     if (lu.nb > kMaxNb) throw Error(MPREC_DIMENSION, "nb > 16 not supported by the ILU kernel");
+    pat->ensure_sched(c);
     flags.ensure(lu.nc);
     MG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * lu.nc, c.s));
     MG_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(int) * 2, c.s));
@@ -173,7 +176,7 @@ void ilu_factor_run(Ctx& c, const BsrView& lu, DBuf<int>& flags, const Pattern* 
         Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * lu.nnzb * lu.nb * lu.nb);
         const int blocks = std::max(1, std::min((lu.nc + kWarps - 1) / kWarps, c.sm_count * 16));
         k_ilu_factor<<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, lu.nc, lu.nb, flags.p, 1,
-                                                       c.counters.p, c.counters.p + 1);
+                                                       pat->fwd.order.p, c.counters.p, c.counters.p + 1);
         check_launch("ilu_factor");
     }
     int zero = 0;

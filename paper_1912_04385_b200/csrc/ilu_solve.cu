@@ -13,7 +13,7 @@
 
 namespace mg {
 
-void ilu_factor_run(Ctx& c, const BsrView& lu, DBuf<int>& flags, const Pattern* pat);
+void ilu_factor_run(Ctx& c, const BsrView& lu, DBuf<int>& flags, Pattern* pat);
 
 namespace {
 
@@ -34,7 +34,9 @@ constexpr int kWarps = 8;
 template <bool kFwd>
 __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp, const int* __restrict__ ci,
                                                       const int* __restrict__ dpos, const double* __restrict__ val,
-                                                      const double* __restrict__ rhs, double* y, int nc, int* counter) {
+                                                      const double* __restrict__ rhs, double* y, int nc,
+                                                      const int* __restrict__ order, int* counter,
+                                                      long long* ts = nullptr) {
     const int lane = threadIdx.x & 31;
     const int r = lane & 7, cq = lane >> 3, c0 = cq * 2;
     for (;;) {
@@ -42,7 +44,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp
         if (lane == 0) t = atomicAdd(counter, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= nc) return;
-        const int I = kFwd ? t : nc - 1 - t;
+        const int I = __ldg(order + t);
         const int d = dpos[I];
         const int ka = kFwd ? rp[I] : d + 1;
         const int kb = kFwd ? d : rp[I + 1];
@@ -90,6 +92,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp
             }
         }
         if (lane < 8) st_pub(y + (int64_t)I * 8 + r, v);
+        if (ts && lane == 0) {
+            long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            ts[2 * t] = g;
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            ts[2 * t + 1] = (long long)smid * 1000000 + (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5));
+        }
     }
 }
 
@@ -98,7 +108,7 @@ template <bool kFwd>
 __global__ void __launch_bounds__(kWarps * 32) k_ilu_gen(const int* __restrict__ rp, const int* __restrict__ ci,
                                                          const int* __restrict__ dpos, const double* __restrict__ val,
                                                          const double* __restrict__ rhs, double* y, int nc, int nb,
-                                                         int* counter) {
+                                                         const int* __restrict__ order, int* counter) {
     const int lane = threadIdx.x & 31;
     const int nb2 = nb * nb;
     for (;;) {
@@ -106,7 +116,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu_gen(const int* __restrict__
         if (lane == 0) t = atomicAdd(counter, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= nc) return;
-        const int I = kFwd ? t : nc - 1 - t;
+        const int I = __ldg(order + t);
         const int d = dpos[I];
         const int ka = kFwd ? rp[I] : d + 1;
         const int kb = kFwd ? d : rp[I + 1];
@@ -114,7 +124,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu_gen(const int* __restrict__
         for (int k = ka; k < kb; ++k) {
             const int K = __ldg(ci + k);
             const double* b = val + (int64_t)k * nb2;
-            const double yk = lane < nb ? ld_poll(y + (int64_t)K * nb + lane) : 0.0;
+            // warp-convergent wait (see amg_cycle.cu)
+            unsigned long long raw = 0;
+            bool pend = lane < nb;
+            while (__any_sync(0xffffffffu, pend)) {
+                if (pend) {
+                    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(raw) : "l"(y + (int64_t)K * nb + lane)
+                                 : "memory");
+                    pend = raw == kPending;
+                }
+            }
+            const double yk = lane < nb ? __longlong_as_double((long long)raw) : 0.0;
             for (int c = 0; c < nb; ++c) {
                 const double yc = __shfl_sync(0xffffffffu, yk, c);
                 if (lane < nb) acc += __ldg(b + c * nb + lane) * yc;
@@ -144,6 +164,9 @@ void Ilu::factor(Ctx& c) { ilu_factor_run(c, lu, flags, pat); }
 
 void Ilu::apply(Ctx& c, const double* r, double* y) {
     const int64_t nn = (int64_t)lu.nc * lu.nb;
+    pat->ensure_sched(c);
+    const int* of = pat->fwd.order.p;
+    const int* ob = pat->bwd.order.p;
     ybuf.ensure(nn);
     // both sweep outputs start as "pending"
     fill_pending(c, ybuf.p, nn);
@@ -158,23 +181,40 @@ void Ilu::apply(Ctx& c, const double* r, double* y) {
     {
         Ctx::Scope sc(&c, MPREC_K_ILU_FWD, bytes);
         if (lu.nb == 8)
-            k_ilu8<true><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, r, ybuf.p, lu.nc,
+            k_ilu8<true><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, r, ybuf.p, lu.nc, of,
                                                           c.counters.p + 2);
         else
             k_ilu_gen<true><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, r, ybuf.p, lu.nc, lu.nb,
-                                                             c.counters.p + 2);
+                                                             of, c.counters.p + 2);
         check_launch("ilu_fwd");
     }
     {
         Ctx::Scope sc(&c, MPREC_K_ILU_BWD, bytes);
         if (lu.nb == 8)
-            k_ilu8<false><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, ybuf.p, y, lu.nc,
+            k_ilu8<false><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, ybuf.p, y, lu.nc, ob,
                                                            c.counters.p + 3);
         else
             k_ilu_gen<false><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, ybuf.p, y, lu.nc,
-                                                              lu.nb, c.counters.p + 3);
+                                                              lu.nb, ob, c.counters.p + 3);
         check_launch("ilu_bwd");
     }
 }
 
+}  // namespace mg
+
+namespace mg {
+// Diagnostics: one forward ILU sweep recording (globaltimer, sm*1e6+warp) per claimed slot.
+void ilu_timeline(Ctx& c, Ilu& ilu, const double* r, double* y, long long* ts_dev, int blocks) {
+    const int64_t nn = (int64_t)ilu.lu.nc * ilu.lu.nb;
+    ilu.pat->ensure_sched(c);
+    ilu.ybuf.ensure(nn);
+    fill_pending(c, ilu.ybuf.p, nn);
+    MG_CUDA(cudaMemsetAsync(c.counters.p + 2, 0, sizeof(int), c.s));
+    if (ilu.lu.nb != 8) throw Error(MPREC_DIMENSION, "timeline diagnostics need nb = 8");
+    if (blocks <= 0) blocks = std::max(1, std::min((ilu.lu.nc + kWarps - 1) / kWarps, c.sm_count * 8));
+    k_ilu8<true><<<blocks, kWarps * 32, 0, c.s>>>(ilu.lu.rp, ilu.lu.ci, ilu.lu.dpos, ilu.lu.val, r, ilu.ybuf.p,
+                                                  ilu.lu.nc, ilu.pat->fwd.order.p, c.counters.p + 2, ts_dev);
+    check_launch("ilu_timeline");
+    c.sync();
+}
 }  // namespace mg

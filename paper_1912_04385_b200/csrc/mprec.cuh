@@ -31,11 +31,29 @@ struct CsrView {
     const int* diag = nullptr;  // position of the diagonal entry per row (square only)
 };
 
-// Block pattern shared by A, Ā and the ILU(0) factors.
+// Topological claim order of a sweep's dependency DAG (sched.cu).
+struct Sched {
+    DBuf<int> order;
+    int n = 0;
+    int nlev = 0;
+};
+// dir = +1: row i depends on stored k < i; dir = -1: on stored k > i.
+void build_sched(Ctx& c, int n, const int* rp, const int* ci, int dir, Sched& out);
+
+// Block pattern shared by A, Ā, the ILU(0) factors and (as a scalar pattern)
+// the level-0 operators B_PP / C_TT of both AMG hierarchies.
 struct Pattern {
     int nc = 0, nnzb = 0;
     DBuf<int> rp, ci, dpos;
     std::vector<int> h_rp, h_ci, h_dpos;
+    Sched fwd, bwd;
+    bool sched_built = false;
+    void ensure_sched(Ctx& c) {
+        if (sched_built) return;
+        build_sched(c, nc, rp.p, ci.p, +1, fwd);
+        build_sched(c, nc, rp.p, ci.p, -1, bwd);
+        sched_built = true;
+    }
 };
 
 // Owned CSR.
@@ -96,7 +114,7 @@ struct Ilu {
     DBuf<double> own;     // factor storage when the Ilu owns it
     DBuf<double> ybuf;    // forward-sweep output
     DBuf<int> flags;      // factorisation ready flags
-    const Pattern* pat = nullptr;
+    Pattern* pat = nullptr;
     int n = 0;
     // factor in place (values of lu are overwritten by L\U); throws ZERO_PIVOT/SETUP
     void factor(Ctx& c);
@@ -117,6 +135,9 @@ struct AmgLevel {
     DCsr a_own, p, r;     // p/r: interpolation into the finer level (levels >= 1)
     DBuf<signed char> cf; // C/F splitting of this level (levels < last)
     DBuf<double> x, b, t, xf, xb;  // work vectors
+    Sched own_fwd, own_bwd;           // Gauss-Seidel claim orders
+    const int* ofwd = nullptr;        // (level 0 may borrow the block pattern's)
+    const int* obwd = nullptr;
 };
 
 struct Amg {
@@ -126,8 +147,9 @@ struct Amg {
     DBuf<double> coarse_lu;   // LU factors (diagnostic / parity)
     int nco = 0;
     DCsr a0_copy;             // when the caller's matrix must be owned
-    // AMGHierarchy::setup (amg.cpp:188-214). a0 must stay alive.
-    void setup(Ctx& c, const CsrView& a0, const AmgParams& p);
+    // AMGHierarchy::setup (amg.cpp:188-214). a0 must stay alive; `pat`
+    // (optional) supplies level 0's sweep schedules when a0 has its pattern.
+    void setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat = nullptr);
     // AMGHierarchy::apply (amg.cpp:233-238): x = V(1,1)-cycle(r), zero initial guess.
     void apply(Ctx& c, const double* r, double* x);
     int n_levels() const { return int(lv.size()); }
@@ -140,7 +162,7 @@ void csr_spmv(Ctx& c, const CsrView& a, const double* x, double* y, const double
               int kclass);
 // forward (dir=+1) / backward (dir=-1) Gauss-Seidel sweep, dependency scheduled
 void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, double* xnew, int dir,
-              bool xold_zero);
+              bool xold_zero, const int* order);
 void dense_gemv(Ctx& c, const double* m_rowmajor, int n, const double* x, double* y);
 
 }  // namespace mg
