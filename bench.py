@@ -44,7 +44,7 @@ KCLASS = ["spmv", "spmv_col", "ilu_fwd", "ilu_bwd", "gs", "csr", "coarse", "mgs"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--steps", type=int, default=1)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=5)
@@ -210,6 +210,36 @@ def ours(args):
     t_gen = time.perf_counter()
     a, b, xs = gen.generate(args.config)
     t_gen = time.perf_counter() - t_gen
+    method_id = {"ilu0": 0, "cpr-amg": 1, "cptr3-amg": 3}[args.method]
+
+    # e2e first (it is also the first warm-up step): solve_system through the C
+    # ABI from HOST buffers -- H2D of A and b, setup, GMRES, D2H of x -- on its
+    # own handle, released before the persistent handle is built (HBM holds one
+    # 30 GB system + its Krylov basis at a time).
+    e2e = None
+    warm_done = 0
+    if not args.no_e2e:
+        x = np.zeros(a.dim)
+        r2 = _Result()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        api.call("solve_system", C.byref(a._c), _ptr(b), method_id, args.tol, args.max_iter, _ptr(x), C.byref(r2))
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([el], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            el = float(tt.item())
+        h2d = a.row_ptr.nbytes + a.col_idx.nbytes + a.values.nbytes + b.nbytes
+        e2e = {"value": world * r2.total_iterations / el, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(x.nbytes), "seconds": el, "setup_s": r2.setup_s, "solve_s": r2.solve_s,
+               "iterations": r2.total_iterations, "timer": "host wall clock around the synchronous C-ABI call",
+               "x_err_vs_xstar": float(np.linalg.norm(x - xs) / np.linalg.norm(xs))}
+        del x
+        warm_done = 1
+
     s = api.system(a).setup(args.method, b)
     stream = C.c_void_p()
     api.call("stream", s.h, C.byref(stream))
@@ -220,7 +250,7 @@ def ours(args):
         api.call("solve_dev", s.h, args.tol, args.max_iter, None, C.byref(res))
         return res.total_iterations, res.converged, res.final_true_residual, res.attempts, res.iterations
 
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup - warm_done, 1 if warm_done == 0 else 0)):
         solve_once()
     # timed region: barrier + sync on both sides, CUDA events on the library stream
     api.call("reset_stats", s.h)
@@ -254,27 +284,6 @@ def ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms = float(tt.item())
     value = world * tot_it / (ms / 1e3)
-
-    # e2e through the C ABI with host buffers
-    e2e = None
-    if not args.no_e2e:
-        x = np.zeros(a.dim)
-        r2 = _Result()
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        api.call("solve_system", C.byref(a._c), _ptr(b), s.method, args.tol, args.max_iter, _ptr(x), C.byref(r2))
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([el], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            el = float(tt.item())
-        h2d = a.row_ptr.nbytes + a.col_idx.nbytes + a.values.nbytes + b.nbytes
-        e2e = {"value": world * r2.total_iterations / el, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(x.nbytes), "seconds": el, "setup_s": r2.setup_s,
-               "iterations": r2.total_iterations, "x_err_vs_xstar": float(np.linalg.norm(x - xs) / np.linalg.norm(xs))}
 
     if rank != 0:
         if world > 1:

@@ -118,7 +118,7 @@ Csr Csr::multiply(const Csr& a, const Csr& b) {
 
 // ===================================================================== Bsr ==
 
-Bsr Bsr::create(int n_cells, int nb, const int* rp, const int* ci, const double* val) {
+Bsr Bsr::create(int n_cells, int nb, const int* rp, const int* ci, const double* val, int missing_diag_code) {
     if (n_cells < 1) throw Error(DIMENSION, "layout needs at least one cell");
     if (nb < 1) throw Error(DIMENSION, "block size must be >= 1");
     if (rp[0] != 0) throw Error(INDEX, "row_ptr[0] must be 0");
@@ -137,7 +137,10 @@ Bsr Bsr::create(int n_cells, int nb, const int* rp, const int* ci, const double*
             if (k > rp[c] && ci[k] <= ci[k - 1]) throw Error(INDEX, "block columns not sorted");
             if (ci[k] == c) m.dpos[c] = k;
         }
-        if (m.dpos[c] < 0) throw Error(DIMENSION, "diagonal block missing in cell " + std::to_string(c), c);
+        if (m.dpos[c] < 0) {
+            if (missing_diag_code == SETUP) throw Error(SETUP, "ILU(0): structurally absent diagonal");
+            throw Error(DIMENSION, "diagonal block missing in cell " + std::to_string(c), c);
+        }
     }
     return m;
 }

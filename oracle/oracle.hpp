@@ -84,7 +84,10 @@ struct Bsr {
     std::vector<int> rp, ci, dpos;
     Vec val;
 
-    static Bsr create(int n_cells, int nb, const int* rp, const int* ci, const double* val);
+    // missing_diag_code: status thrown for a structurally absent diagonal block
+    // (DIMENSION for a system; SETUP for ILU0Factor::factor, ilu0.cpp:20)
+    static Bsr create(int n_cells, int nb, const int* rp, const int* ci, const double* val,
+                      int missing_diag_code = DIMENSION);
     int dim() const { return nc * nb; }
     double& at(int64_t k, int r, int c) { return val[(k * nb + c) * nb + r]; }
     double at(int64_t k, int r, int c) const { return val[(k * nb + c) * nb + r]; }

@@ -50,7 +50,9 @@ Csr to_csr(const mprec_csr* a) {
     return m;
 }
 
-Bsr to_bsr(const mprec_bsr* a) { return Bsr::create(a->n_cells, a->nb, a->row_ptr, a->col_idx, a->values); }
+Bsr to_bsr(const mprec_bsr* a, int missing_diag_code = DIMENSION) {
+    return Bsr::create(a->n_cells, a->nb, a->row_ptr, a->col_idx, a->values, missing_diag_code);
+}
 
 double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -265,7 +267,7 @@ int orc_ilu_create(const mprec_bsr* a, orc_ilu** out) {
     return guard([&] {
         auto* h = new orc_ilu;
         try {
-            h->f = Ilu0Block::factor(to_bsr(a));
+            h->f = Ilu0Block::factor(to_bsr(a, SETUP));
         } catch (...) {
             delete h;
             throw;

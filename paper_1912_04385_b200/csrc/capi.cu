@@ -45,7 +45,8 @@ double now_s() {
 }
 
 // Validates a canonical BSR (block_matrix.cpp:32-69 invariants) and uploads the pattern.
-void load_pattern(Ctx& c, Pattern& p, int nc, int nb, const int* rp, const int* ci) {
+void load_pattern(Ctx& c, Pattern& p, int nc, int nb, const int* rp, const int* ci,
+                  int missing_diag_code = MPREC_DIMENSION) {
     if (nc < 1) throw Error(MPREC_DIMENSION, "layout needs at least one cell");
     if (nb < 1) throw Error(MPREC_DIMENSION, "block size must be >= 1");
     if (!rp || !ci) throw Error(MPREC_DIMENSION, "null pattern");
@@ -62,8 +63,10 @@ void load_pattern(Ctx& c, Pattern& p, int nc, int nb, const int* rp, const int* 
             if (k > rp[r] && ci[k] <= ci[k - 1]) throw Error(MPREC_INDEX, "block columns not sorted");
             if (ci[k] == r) p.h_dpos[r] = k;
         }
-        if (p.h_dpos[r] < 0)
+        if (p.h_dpos[r] < 0) {
+            if (missing_diag_code == MPREC_SETUP) throw Error(MPREC_SETUP, "ILU(0): structurally absent diagonal");
             throw Error(MPREC_DIMENSION, "diagonal block missing in cell " + std::to_string(r), r);
+        }
     }
     p.rp.upload(p.h_rp.data(), p.h_rp.size(), c.s);
     p.ci.upload(p.h_ci.data(), std::max<size_t>(p.h_ci.size(), 1), c.s);
@@ -699,7 +702,7 @@ int mprec_gpu_ilu_create(const mprec_bsr* a, mprec_gpu_ilu** out) {
     return guard([&] {
         if (!a || !out) throw Error(MPREC_DIMENSION, "null argument");
         auto h = std::make_unique<mprec_gpu_ilu>();
-        load_pattern(h->ctx, h->pat, a->n_cells, a->nb, a->row_ptr, a->col_idx);
+        load_pattern(h->ctx, h->pat, a->n_cells, a->nb, a->row_ptr, a->col_idx, MPREC_SETUP);
         const size_t nv = std::max<size_t>(size_t(h->pat.nnzb) * a->nb * a->nb, 1);
         h->vals.upload(a->values, nv, h->ctx.s);
         h->ilu.lu = view_of(h->pat, a->nb, h->vals.p);
