@@ -228,12 +228,10 @@ def ours(args):
         api.call("solve_system", C.byref(a._c), _ptr(b), method_id, args.tol, args.max_iter, _ptr(x), C.byref(r2))
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([el], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            el = float(tt.item())
+        from paper_1912_04385_b200 import replicas
+        el = replicas.reduce_max(el, dev)
         h2d = a.row_ptr.nbytes + a.col_idx.nbytes + a.values.nbytes + b.nbytes
-        e2e = {"value": world * r2.total_iterations / el, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": replicas.reduce_sum(r2.total_iterations, dev) / el, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(x.nbytes), "seconds": el, "setup_s": r2.setup_s, "solve_s": r2.solve_s,
                "iterations": r2.total_iterations, "timer": "host wall clock around the synchronous C-ABI call",
                "x_err_vs_xstar": float(np.linalg.norm(x - xs) / np.linalg.norm(xs))}
@@ -279,11 +277,9 @@ def ours(args):
         api.call("kernel_stats", s.h, k, C.byref(t), C.byref(n), C.byref(by))
         stats[name] = {"ms": t.value, "launches": n.value, "bytes": by.value}
     api.call("profile", s.h, 0)
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
-    value = world * tot_it / (ms / 1e3)
+    from paper_1912_04385_b200 import replicas
+    ms = replicas.reduce_max(ms, dev)
+    value = replicas.reduce_sum(tot_it, dev) / (ms / 1e3)
 
     if rank != 0:
         if world > 1:

@@ -9,6 +9,8 @@
 // order from an atomic counter, the new iterate is written to a fresh buffer
 // pre-filled with the kPending sentinel and consumers poll the producer's value
 // (double buffering also makes the "old" reads race-free for any pattern).
+#include <cstdlib>
+
 #include "mprec.cuh"
 
 namespace mg {
@@ -34,7 +36,7 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp
                                                       const double* __restrict__ v, const int* __restrict__ diag,
                                                       const double* __restrict__ b, const double* __restrict__ xold,
                                                       double* xnew, int n, const int* __restrict__ order,
-                                                      int* counter) {
+                                                      int* counter, unsigned sleep_ns) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         int t = 0;
@@ -62,6 +64,7 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp
                     raw = ld_relaxed(xnew + j);
                     pend = raw == kPending;
                 }
+                if (sleep_ns && __any_sync(0xffffffffu, pend)) __nanosleep(sleep_ns);
             }
             if (dep) xj = __longlong_as_double((long long)raw);
             acc += a * xj;
@@ -109,13 +112,21 @@ void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, dou
     Ctx::Scope sc(&c, MPREC_K_GS, bytes);
     int* ctr = c.counters.p + 4;
     MG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), c.s));
-    const int blocks = std::max(1, std::min((a.n + kGsWarps - 1) / kGsWarps, c.sm_count * 8));
+    static const int blk_per_sm = [] {
+        const char* e = getenv("MPREC_GS_BLOCKS_PER_SM");
+        return e ? atoi(e) : 8;
+    }();
+    static const unsigned sleep_ns = [] {
+        const char* e = getenv("MPREC_POLL_SLEEP");
+        return e ? unsigned(atoi(e)) : 0u;
+    }();
+    const int blocks = std::max(1, std::min((a.n + kGsWarps - 1) / kGsWarps, c.sm_count * blk_per_sm));
     if (dir > 0)
         k_gs<1><<<blocks, kGsWarps * 32, 0, c.s>>>(a.rp, a.ci, a.v, a.diag, b, xold_zero ? nullptr : xold, xnew, a.n,
-                                                   order, ctr);
+                                                   order, ctr, sleep_ns);
     else
         k_gs<-1><<<blocks, kGsWarps * 32, 0, c.s>>>(a.rp, a.ci, a.v, a.diag, b, xold_zero ? nullptr : xold, xnew,
-                                                    a.n, order, ctr);
+                                                    a.n, order, ctr, sleep_ns);
     check_launch("gs_sweep");
 }
 
@@ -167,4 +178,39 @@ void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
 // amg.cpp:233-238
 void Amg::apply(Ctx& c, const double* r, double* x) { cycle(c, 0, r, x); }
 
+}  // namespace mg
+
+namespace mg {
+// Diagnostics: time `reps` forward+backward sweeps on level l of an AMG.
+void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int* nl_f, int* nl_b) {
+    AmgLevel& L = *amg.lv[l];
+    fill(c, L.b.p, 1.0, L.n);
+    cudaEvent_t e0, e1, e2;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
+    float tf = 0, tb = 0;
+    for (int r = 0; r < reps; ++r) {
+        fill_pending(c, L.xf.p, L.n);
+        fill_pending(c, L.x.p, L.n);
+        cudaEventRecord(e0, c.s);
+        gs_sweep(c, L.a, L.b.p, nullptr, L.xf.p, +1, true, L.ofwd);
+        cudaEventRecord(e1, c.s);
+        gs_sweep(c, L.a, L.b.p, L.xf.p, L.x.p, -1, false, L.obwd);
+        cudaEventRecord(e2, c.s);
+        cudaEventSynchronize(e2);
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, e0, e1);
+        cudaEventElapsedTime(&b, e1, e2);
+        tf += a;
+        tb += b;
+    }
+    *ms_f = tf / reps;
+    *ms_b = tb / reps;
+    *nl_f = L.own_fwd.nlev;
+    *nl_b = L.own_bwd.nlev;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+}
 }  // namespace mg

@@ -12,6 +12,8 @@
 #include <cstring>
 #include <functional>
 
+#include <cuda_profiler_api.h>
+
 #include "mprec.cuh"
 
 using namespace mg;
@@ -256,6 +258,7 @@ void fill_result(mprec_solve_result* r, const GmresOut& g, int attempts, double 
 
 namespace mg {
 void ilu_timeline(Ctx& c, Ilu& ilu, const double* r, double* y, long long* ts_dev, int blocks);
+void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int* nl_f, int* nl_b);
 }
 
 // ============================================================ AMG handle ==
@@ -352,6 +355,20 @@ struct mprec_gpu_system {
     int total_iterations = 0;
     GmresOut solve_attempts(double tol, int max_iter, double* xdev, int* attempts) {
         Ctx& c = ctx;
+        // MPREC_PROFILE_SOLVE=1: bracket the solve for `ncu --profile-from-start off`
+        static const bool prof = [] {
+            const char* e = getenv("MPREC_PROFILE_SOLVE");
+            return e && e[0] == '1';
+        }();
+        struct ProfRange {
+            bool on;
+            explicit ProfRange(bool o) : on(o) {
+                if (on) cudaProfilerStart();
+            }
+            ~ProfRange() {
+                if (on) cudaProfilerStop();
+            }
+        } pr(prof);
         const DevOp Aop = [this](const double* xx, double* yy) { bsr_spmv(ctx, Abar(), xx, yy, nullptr, MPREC_K_SPMV); };
         const DevOp Mop = [this](const double* xx, double* yy) { prec_apply(xx, yy); };
         double bn = 0.0;
@@ -800,6 +817,21 @@ int mprec_gpu_debug_ilu_timeline(mprec_gpu_system* h, int blocks, long long* ts,
         h->pat.fwd.order.download(order, h->pat.nc, h->ctx.s);
         *nlev = h->pat.fwd.nlev;
         h->ctx.sync();
+    });
+}
+
+// Diagnostics: sweep timing on one AMG level (stage as in mprec_gpu_stage_amg).
+int mprec_gpu_debug_gs(mprec_gpu_system* h, int stage, int level, int reps, double* ms_f, double* ms_b, int* nl_f,
+                       int* nl_b) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        Amg* a = (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) ? h->amgT.get() : h->amgP.get();
+        if (level < 0 || level + 1 >= a->n_levels()) throw Error(MPREC_INDEX, "level out of range");
+        gs_bench(h->ctx, *a, level, reps, ms_f, ms_b, nl_f, nl_b);
+        if (level == 0) {
+            *nl_f = h->pat.fwd.nlev;
+            *nl_b = h->pat.bwd.nlev;
+        }
     });
 }
 
