@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp
                                                       const double* __restrict__ v, const int* __restrict__ diag,
                                                       const double* __restrict__ b, const double* __restrict__ xold,
                                                       double* xnew, int n, const int* __restrict__ order,
-                                                      int* counter, unsigned sleep_ns) {
+                                                      int* counter, unsigned sleep_ns, const double* __restrict__ invd) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         int t = 0;
@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp
         const int i = __ldg(order + t);
         const int k0 = __ldg(rp + i), k1 = __ldg(rp + i + 1);
         // independent of the dependency chain: issue before waiting
-        const double bi = __ldg(b + i), dii = __ldg(v + __ldg(diag + i));
+        const double bi = __ldg(b + i);
+        const double dii = invd ? __ldg(invd + i) : __ldg(v + __ldg(diag + i));
         double acc = 0.0;
         for (int base = k0; base < k1; base += 32) {
             const int k = base + lane;
@@ -71,8 +72,13 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) st_pub(xnew + i, (bi - acc) / dii);
+        if (lane == 0) st_pub(xnew + i, invd ? (bi - acc) * dii : (bi - acc) / dii);
     }
+}
+
+__global__ void k_invd(const double* v, const int* diag, int n, double* invd) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) invd[i] = 1.0 / v[diag[i]];
 }
 
 // 8 lanes per row; mode 0: y = Ax, 1: y = b - Ax, 2: y = y + Ax
@@ -107,7 +113,7 @@ __global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ m, int 
 }  // namespace
 
 void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, double* xnew, int dir, bool xold_zero,
-              const int* order) {
+              const int* order, const double* invd) {
     const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 4.0 * a.n + 24.0 * a.n;
     Ctx::Scope sc(&c, MPREC_K_GS, bytes);
     int* ctr = c.counters.p + 4;
@@ -123,11 +129,16 @@ void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, dou
     const int blocks = std::max(1, std::min((a.n + kGsWarps - 1) / kGsWarps, c.sm_count * blk_per_sm));
     if (dir > 0)
         k_gs<1><<<blocks, kGsWarps * 32, 0, c.s>>>(a.rp, a.ci, a.v, a.diag, b, xold_zero ? nullptr : xold, xnew, a.n,
-                                                   order, ctr, sleep_ns);
+                                                   order, ctr, sleep_ns, invd);
     else
         k_gs<-1><<<blocks, kGsWarps * 32, 0, c.s>>>(a.rp, a.ci, a.v, a.diag, b, xold_zero ? nullptr : xold, xnew,
-                                                    a.n, order, ctr, sleep_ns);
+                                                    a.n, order, ctr, sleep_ns, invd);
     check_launch("gs_sweep");
+}
+
+void compute_invd(Ctx& c, const CsrView& a, double* invd) {
+    k_invd<<<(a.n + 255) / 256, 256, 0, c.s>>>(a.v, a.diag, a.n, invd);
+    check_launch("invd");
 }
 
 void csr_spmv(Ctx& c, const CsrView& a, const double* x, double* y, const double* b, bool add_to_y, int kclass) {
@@ -148,6 +159,15 @@ void dense_gemv(Ctx& c, const double* m, int n, const double* x, double* y) {
     check_launch("dense_gemv");
 }
 
+// one Gauss-Seidel direction on level L: band schedule when available
+static void level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold, double* xnew, int dir, bool zero) {
+    const BandSched& bs = dir > 0 ? L.band_fwd : L.band_bwd;
+    if (bs.ok)
+        gs_band_sweep(c, bs, L.a.nnz, L.n, r, zero ? nullptr : xold, xnew);
+    else
+        gs_sweep(c, L.a, r, xold, xnew, dir, zero, dir > 0 ? L.ofwd : L.obwd, L.invd.p);
+}
+
 // amg.cpp:216-231
 void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
     AmgLevel& L = *lv[l];
@@ -159,9 +179,9 @@ void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
     const int64_t n = L.n;
     // x = 0; sym GS
     fill_pending(c, L.xf.p, n);
-    gs_sweep(c, L.a, r, nullptr, L.xf.p, +1, true, L.ofwd);
+    level_sweep(c, L, r, nullptr, L.xf.p, +1, true);
     fill_pending(c, x, n);
-    gs_sweep(c, L.a, r, L.xf.p, x, -1, false, L.obwd);
+    level_sweep(c, L, r, L.xf.p, x, -1, false);
     // rc = R (r - A x)
     csr_spmv(c, L.a, x, L.t.p, r, false, MPREC_K_CSR);
     csr_spmv(c, N.r.view(), L.t.p, N.b.p, nullptr, false, MPREC_K_CSR);
@@ -170,9 +190,9 @@ void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
     csr_spmv(c, N.p.view(), N.x.p, x, nullptr, true, MPREC_K_CSR);
     // post sym GS
     fill_pending(c, L.xf.p, n);
-    gs_sweep(c, L.a, r, x, L.xf.p, +1, false, L.ofwd);
+    level_sweep(c, L, r, x, L.xf.p, +1, false);
     fill_pending(c, x, n);
-    gs_sweep(c, L.a, r, L.xf.p, x, -1, false, L.obwd);
+    level_sweep(c, L, r, L.xf.p, x, -1, false);
 }
 
 // amg.cpp:233-238
@@ -181,6 +201,22 @@ void Amg::apply(Ctx& c, const double* r, double* x) { cycle(c, 0, r, x); }
 }  // namespace mg
 
 namespace mg {
+extern long long* g_band_ts;
+// Diagnostics: per-band timeline of one forward band sweep on level l
+void gs_band_timeline(Ctx& c, Amg& amg, int l, long long* host_ts, int* nbands) {
+    AmgLevel& L = *amg.lv[l];
+    if (!L.band_fwd.ok) throw Error(MPREC_SETUP, "no band schedule on this level");
+    DBuf<long long> ts(3 * L.band_fwd.nbands + 2 * L.band_fwd.nchunks);
+    fill(c, L.b.p, 1.0, L.n);
+    fill_pending(c, L.xf.p, L.n);
+    g_band_ts = ts.p;
+    level_sweep(c, L, L.b.p, nullptr, L.xf.p, +1, true);
+    c.sync();
+    g_band_ts = nullptr;
+    ts.download(host_ts, 3 * L.band_fwd.nbands + 2 * L.band_fwd.nchunks, c.s);
+    c.sync();
+    *nbands = L.band_fwd.nbands;
+}
 // Diagnostics: time `reps` forward+backward sweeps on level l of an AMG.
 void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int* nl_f, int* nl_b) {
     AmgLevel& L = *amg.lv[l];
@@ -194,9 +230,9 @@ void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int
         fill_pending(c, L.xf.p, L.n);
         fill_pending(c, L.x.p, L.n);
         cudaEventRecord(e0, c.s);
-        gs_sweep(c, L.a, L.b.p, nullptr, L.xf.p, +1, true, L.ofwd);
+        level_sweep(c, L, L.b.p, nullptr, L.xf.p, +1, true);
         cudaEventRecord(e1, c.s);
-        gs_sweep(c, L.a, L.b.p, L.xf.p, L.x.p, -1, false, L.obwd);
+        level_sweep(c, L, L.b.p, L.xf.p, L.x.p, -1, false);
         cudaEventRecord(e2, c.s);
         cudaEventSynchronize(e2);
         float a = 0, b = 0;
@@ -207,8 +243,8 @@ void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int
     }
     *ms_f = tf / reps;
     *ms_b = tb / reps;
-    *nl_f = L.own_fwd.nlev;
-    *nl_b = L.own_bwd.nlev;
+    *nl_f = L.band_fwd.ok ? -L.band_fwd.nbands : L.own_fwd.nlev;
+    *nl_b = L.band_bwd.ok ? -L.band_bwd.nbands : L.own_bwd.nlev;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);

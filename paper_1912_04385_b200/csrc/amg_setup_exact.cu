@@ -25,6 +25,7 @@
 //  * Galerkin R(AP) (scalar_matrix.cpp:120-151): per output entry the products
 //    are summed from 0.0 in ascending A-column order, symbolic zeros kept.
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "mprec.cuh"
 
@@ -903,7 +904,24 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
                 l.ofwd = l.own_fwd.order.p;
                 l.obwd = l.own_bwd.order.p;
             }
+            l.invd.alloc(std::max(l.n, 1));
+            compute_invd(c, l.a, l.invd.p);
         }
+    }
+    {
+        static const bool band_on = [] {
+            const char* e = getenv("MPREC_GS_BAND");
+            return e && e[0] == '1';  // opt-in
+        }();
+        Trace tr(&c, "amg band schedules");
+        if (band_on)
+            for (size_t li = 0; li + 1 < lv.size(); ++li) {
+                AmgLevel& l = *lv[li];
+                const int* gf = (li == 0 && pat) ? pat->fwd.level.p : l.own_fwd.level.p;
+                const int* gb = (li == 0 && pat) ? pat->bwd.level.p : l.own_bwd.level.p;
+                build_band_sched(c, l.a, +1, gf, l.band_fwd);
+                build_band_sched(c, l.a, -1, gb, l.band_bwd);
+            }
     }
     for (auto& l : lv) {
         l->x.ensure(std::max(l->n, 1));

@@ -259,6 +259,7 @@ void fill_result(mprec_solve_result* r, const GmresOut& g, int attempts, double 
 namespace mg {
 void ilu_timeline(Ctx& c, Ilu& ilu, const double* r, double* y, long long* ts_dev, int blocks);
 void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int* nl_f, int* nl_b);
+void gs_band_timeline(Ctx& c, Amg& amg, int l, long long* host_ts, int* nbands);
 }
 
 // ============================================================ AMG handle ==
@@ -828,10 +829,18 @@ int mprec_gpu_debug_gs(mprec_gpu_system* h, int stage, int level, int reps, doub
         Amg* a = (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) ? h->amgT.get() : h->amgP.get();
         if (level < 0 || level + 1 >= a->n_levels()) throw Error(MPREC_INDEX, "level out of range");
         gs_bench(h->ctx, *a, level, reps, ms_f, ms_b, nl_f, nl_b);
-        if (level == 0) {
+        if (level == 0 && *nl_f >= 0) {
             *nl_f = h->pat.fwd.nlev;
             *nl_b = h->pat.bwd.nlev;
         }
+    });
+}
+
+int mprec_gpu_debug_band_timeline(mprec_gpu_system* h, int stage, int level, long long* ts, int* nbands) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        Amg* a = (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) ? h->amgT.get() : h->amgP.get();
+        gs_band_timeline(h->ctx, *a, level, ts, nbands);
     });
 }
 

@@ -17,12 +17,10 @@ void ilu_factor_run(Ctx& c, const BsrView& lu, DBuf<int>& flags, Pattern* pat);
 
 namespace {
 
-__device__ __forceinline__ double ld_poll(const double* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed(const double* p) {
     unsigned long long v;
-    do {
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    } while (v == kPending);
-    return __longlong_as_double((long long)v);
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ void st_pub(double* p, double v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
@@ -36,7 +34,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp
                                                       const int* __restrict__ dpos, const double* __restrict__ val,
                                                       const double* __restrict__ rhs, double* y, int nc,
                                                       const int* __restrict__ order, int* counter,
-                                                      long long* ts = nullptr) {
+                                                      const double* __restrict__ dinv, long long* ts = nullptr) {
     const int lane = threadIdx.x & 31;
     const int r = lane & 7, cq = lane >> 3, c0 = cq * 2;
     for (;;) {
@@ -48,50 +46,70 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp
         const int d = dpos[I];
         const int ka = kFwd ? rp[I] : d + 1;
         const int kb = kFwd ? d : rp[I + 1];
-        // diagonal block row r (all 8 columns) -- independent of the chain
-        const double* bd = val + (int64_t)d * 64;
+        // row r of the packed inverse diagonal block (strict lower: inv(L_II),
+        // upper incl. diagonal: inv(U_II)) -- independent of the chain
+        const double* bd = dinv + (int64_t)I * 64;
         double drow[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) drow[c] = __ldg(bd + c * 8 + r);
         double acc = 0.0;
-        int k = ka;
-        for (; k + 2 <= kb; k += 2) {
-            const int K0 = __ldg(ci + k), K1 = __ldg(ci + k + 1);
-            const double* b0 = val + (int64_t)k * 64;
-            const double* b1 = b0 + 64;
-            const double v00 = __ldg(b0 + c0 * 8 + r), v01 = __ldg(b0 + (c0 + 1) * 8 + r);
-            const double v10 = __ldg(b1 + c0 * 8 + r), v11 = __ldg(b1 + (c0 + 1) * 8 + r);
-            const double y00 = ld_poll(y + (int64_t)K0 * 8 + c0), y01 = ld_poll(y + (int64_t)K0 * 8 + c0 + 1);
-            const double y10 = ld_poll(y + (int64_t)K1 * 8 + c0), y11 = ld_poll(y + (int64_t)K1 * 8 + c0 + 1);
-            acc += v00 * y00 + v01 * y01;
-            acc += v10 * y10 + v11 * y11;
-        }
-        for (; k < kb; ++k) {
-            const int K = __ldg(ci + k);
-            const double* b0 = val + (int64_t)k * 64;
-            const double v0 = __ldg(b0 + c0 * 8 + r), v1 = __ldg(b0 + (c0 + 1) * 8 + r);
-            const double y0 = ld_poll(y + (int64_t)K * 8 + c0), y1 = ld_poll(y + (int64_t)K * 8 + c0 + 1);
-            acc += v0 * y0 + v1 * y1;
+        // dependency blocks in groups of 4: block values first, then ALL polls
+        // issued together, then a warp-convergent re-poll of the pending ones
+        for (int kk = ka; kk < kb; kk += 4) {
+            double va[4][2];
+            unsigned long long raw[4][2];
+            int K[4];
+            bool pend[4][2];
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool ok = kk + u < kb;
+                K[u] = ok ? __ldg(ci + kk + u) : 0;
+                const double* bk = val + (int64_t)(ok ? kk + u : ka) * 64;
+                va[u][0] = ok ? __ldg(bk + c0 * 8 + r) : 0.0;
+                va[u][1] = ok ? __ldg(bk + (c0 + 1) * 8 + r) : 0.0;
+                pend[u][0] = pend[u][1] = ok;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    raw[u][h] = pend[u][h] ? ld_relaxed(y + (int64_t)K[u] * 8 + c0 + h) : 0ull;
+                    pend[u][h] = pend[u][h] && raw[u][h] == kPending;
+                    any |= pend[u][h];
+                }
+            while (__any_sync(0xffffffffu, any)) {
+                any = false;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (pend[u][h]) {
+                            raw[u][h] = ld_relaxed(y + (int64_t)K[u] * 8 + c0 + h);
+                            pend[u][h] = raw[u][h] == kPending;
+                            any |= pend[u][h];
+                        }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                acc += va[u][0] * __longlong_as_double((long long)raw[u][0]) +
+                       va[u][1] * __longlong_as_double((long long)raw[u][1]);
         }
         acc += __shfl_xor_sync(0xffffffffu, acc, 8);
         acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-        double v = rhs[(int64_t)I * 8 + r] - acc;
-        if (kFwd) {
-            // unit lower triangular diagonal block
+        const double v = rhs[(int64_t)I * 8 + r] - acc;
+        // y_I = inv(L_II) v (forward) or inv(U_II) v (backward): 8 independent
+        // shuffles + FMAs instead of an 8-step serial substitution
+        double yv[8];
 #pragma unroll
-            for (int c = 0; c < 7; ++c) {
-                const double yc = __shfl_sync(0xffffffffu, v, c);
-                if (r > c) v -= drow[c] * yc;
-            }
-        } else {
+        for (int c = 0; c < 8; ++c) yv[c] = __shfl_sync(0xffffffffu, v, c);
+        double out = kFwd ? yv[r] : 0.0;
 #pragma unroll
-            for (int c = 7; c >= 0; --c) {
-                if (r == c) v = v / drow[c];
-                const double yc = __shfl_sync(0xffffffffu, v, c);
-                if (r < c) v -= drow[c] * yc;
-            }
+        for (int c = 0; c < 8; ++c) {
+            if (kFwd ? (c < r) : (c >= r)) out += drow[c] * yv[c];
         }
-        if (lane < 8) st_pub(y + (int64_t)I * 8 + r, v);
+        const double v_out = out;
+        if (lane < 8) st_pub(y + (int64_t)I * 8 + r, v_out);
         if (ts && lane == 0) {
             long long g;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -158,9 +176,50 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu_gen(const int* __restrict__
     }
 }
 
+// packed inverse diagonal blocks: strict lower = inv(unit L_II), upper = inv(U_II)
+__global__ void k_ilu_dinv8(const int* __restrict__ dpos, const double* __restrict__ val, int nc, double* dinv) {
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= nc) return;
+    const double* d = val + (int64_t)dpos[I] * 64;
+    double m[64], o[64];
+#pragma unroll
+    for (int e = 0; e < 64; ++e) {
+        m[e] = d[e];
+        o[e] = 0.0;
+    }
+    // inv(L) column by column: L unit lower (strict part of m)
+    for (int j = 0; j < 8; ++j) {
+        double x[8];
+        for (int i = 0; i < 8; ++i) x[i] = (i == j) ? 1.0 : 0.0;
+        for (int k = 0; k < 8; ++k)
+            for (int i = k + 1; i < 8; ++i) x[i] -= m[k * 8 + i] * x[k];
+        for (int i = j + 1; i < 8; ++i) o[j * 8 + i] = x[i];
+    }
+    // inv(U) column by column: U upper incl. diagonal
+    for (int j = 0; j < 8; ++j) {
+        double x[8];
+        for (int i = 0; i < 8; ++i) x[i] = (i == j) ? 1.0 : 0.0;
+        for (int k = 7; k >= 0; --k) {
+            x[k] /= m[k * 8 + k];
+            for (int i = 0; i < k; ++i) x[i] -= m[k * 8 + i] * x[k];
+        }
+        for (int i = 0; i <= j; ++i) o[j * 8 + i] = x[i];
+    }
+    double* out = dinv + (int64_t)I * 64;
+#pragma unroll
+    for (int e = 0; e < 64; ++e) out[e] = o[e];
+}
+
 }  // namespace
 
-void Ilu::factor(Ctx& c) { ilu_factor_run(c, lu, flags, pat); }
+void Ilu::factor(Ctx& c) {
+    ilu_factor_run(c, lu, flags, pat);
+    if (lu.nb == 8) {
+        dinv.ensure((size_t)lu.nc * 64);
+        k_ilu_dinv8<<<(lu.nc + 127) / 128, 128, 0, c.s>>>(lu.dpos, lu.val, lu.nc, dinv.p);
+        check_launch("ilu dinv");
+    }
+}
 
 void Ilu::apply(Ctx& c, const double* r, double* y) {
     const int64_t nn = (int64_t)lu.nc * lu.nb;
@@ -182,7 +241,7 @@ void Ilu::apply(Ctx& c, const double* r, double* y) {
         Ctx::Scope sc(&c, MPREC_K_ILU_FWD, bytes);
         if (lu.nb == 8)
             k_ilu8<true><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, r, ybuf.p, lu.nc, of,
-                                                          c.counters.p + 2);
+                                                          c.counters.p + 2, dinv.p);
         else
             k_ilu_gen<true><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, r, ybuf.p, lu.nc, lu.nb,
                                                              of, c.counters.p + 2);
@@ -192,7 +251,7 @@ void Ilu::apply(Ctx& c, const double* r, double* y) {
         Ctx::Scope sc(&c, MPREC_K_ILU_BWD, bytes);
         if (lu.nb == 8)
             k_ilu8<false><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, ybuf.p, y, lu.nc, ob,
-                                                           c.counters.p + 3);
+                                                           c.counters.p + 3, dinv.p);
         else
             k_ilu_gen<false><<<blocks, kWarps * 32, 0, c.s>>>(lu.rp, lu.ci, lu.dpos, lu.val, ybuf.p, y, lu.nc,
                                                               lu.nb, ob, c.counters.p + 3);
@@ -213,7 +272,8 @@ void ilu_timeline(Ctx& c, Ilu& ilu, const double* r, double* y, long long* ts_de
     if (ilu.lu.nb != 8) throw Error(MPREC_DIMENSION, "timeline diagnostics need nb = 8");
     if (blocks <= 0) blocks = std::max(1, std::min((ilu.lu.nc + kWarps - 1) / kWarps, c.sm_count * 8));
     k_ilu8<true><<<blocks, kWarps * 32, 0, c.s>>>(ilu.lu.rp, ilu.lu.ci, ilu.lu.dpos, ilu.lu.val, r, ilu.ybuf.p,
-                                                  ilu.lu.nc, ilu.pat->fwd.order.p, c.counters.p + 2, ts_dev);
+                                                  ilu.lu.nc, ilu.pat->fwd.order.p, c.counters.p + 2, ilu.dinv.p,
+                                                  ts_dev);
     check_launch("ilu_timeline");
     c.sync();
 }

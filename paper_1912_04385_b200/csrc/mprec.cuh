@@ -34,6 +34,7 @@ struct CsrView {
 // Topological claim order of a sweep's dependency DAG (sched.cu).
 struct Sched {
     DBuf<int> order;
+    DBuf<int> level;  // DAG level (Kahn round) of every row
     int n = 0;
     int nlev = 0;
 };
@@ -114,6 +115,7 @@ struct Ilu {
     DBuf<double> own;     // factor storage when the Ilu owns it
     DBuf<double> ybuf;    // forward-sweep output
     DBuf<int> flags;      // factorisation ready flags
+    DBuf<double> dinv;    // nb = 8: packed inverses of the diagonal blocks (apply path)
     Pattern* pat = nullptr;
     int n = 0;
     // factor in place (values of lu are overwritten by L\U); throws ZERO_PIVOT/SETUP
@@ -129,6 +131,21 @@ struct AmgParams {
     int max_levels = 25;
 };
 
+// Band ("doacross") schedule of one Gauss-Seidel sweep direction (gs_band.cu).
+struct BandSched {
+    bool ok = false;
+    int B = 0, nbands = 0, nchunks = 0, slot_bytes = 0, rec_max = 0, depth = 0, dir = 0, smem = 0, nlev_total = 0;
+    DBuf<int4> chunks;
+    DBuf<long long> coff;
+    DBuf<int> band_chunk, band_recb;
+    DBuf<unsigned char> rec;
+};
+// `glev`: global DAG levels of the same direction (sched.cu); rows of a band are
+// processed in global-level order so consecutive bands advance in lockstep.
+bool build_band_sched(Ctx& c, const CsrView& a, int dir, const int* glev, BandSched& s);
+void gs_band_sweep(Ctx& c, const BandSched& s, int64_t nnz, int n, const double* b, const double* xold,
+                   double* xnew);
+
 struct AmgLevel {
     int n = 0;
     CsrView a;            // level operator (level 0 may be a non-owning view)
@@ -138,6 +155,8 @@ struct AmgLevel {
     Sched own_fwd, own_bwd;           // Gauss-Seidel claim orders
     const int* ofwd = nullptr;        // (level 0 may borrow the block pattern's)
     const int* obwd = nullptr;
+    BandSched band_fwd, band_bwd;     // band schedules (opt-in, MPREC_GS_BAND=1)
+    DBuf<double> invd;                // 1 / a_ii
 };
 
 struct Amg {
@@ -161,8 +180,10 @@ struct Amg {
 void csr_spmv(Ctx& c, const CsrView& a, const double* x, double* y, const double* b, bool add_to_y,
               int kclass);
 // forward (dir=+1) / backward (dir=-1) Gauss-Seidel sweep, dependency scheduled
+// invd (optional): precomputed 1/a_ii (multiply instead of the fp64 division)
 void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, double* xnew, int dir,
-              bool xold_zero, const int* order);
+              bool xold_zero, const int* order, const double* invd = nullptr);
 void dense_gemv(Ctx& c, const double* m_rowmajor, int n, const double* x, double* y);
+void compute_invd(Ctx& c, const CsrView& a, double* invd);
 
 }  // namespace mg

@@ -44,9 +44,12 @@ __global__ void k_dep_fill(const int* rp, const int* ci, int n, int dir, const i
     }
 }
 
-__global__ void k_zero_flag(const int* indeg, int n, int* flag) {
+__global__ void k_zero_flag(const int* indeg, int n, int* flag, int* lev) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flag[i] = indeg[i] == 0 ? 1 : 0;
+    if (i < n) {
+        flag[i] = indeg[i] == 0 ? 1 : 0;
+        lev[i] = 0;
+    }
 }
 
 __global__ void k_compact(const int* flag, const int* pos, int n, int* out) {
@@ -55,13 +58,16 @@ __global__ void k_compact(const int* flag, const int* pos, int n, int* out) {
 }
 
 // st[0] = begin, st[1] = end of the current frontier, st[2] = tail, st[3] = rounds
-__global__ void k_round(const int* drp, const int* dci, int* indeg, int* order, int* st) {
-    const int b = st[0], e = st[1];
+__global__ void k_round(const int* drp, const int* dci, int* indeg, int* order, int* st, int* lev) {
+    const int b = st[0], e = st[1], L = st[3];
     for (int t = b + blockIdx.x * blockDim.x + threadIdx.x; t < e; t += gridDim.x * blockDim.x) {
         const int r = order[t];
         for (int k = drp[r]; k < drp[r + 1]; ++k) {
             const int i = dci[k];
-            if (atomicSub(indeg + i, 1) == 1) order[atomicAdd(st + 2, 1)] = i;
+            if (atomicSub(indeg + i, 1) == 1) {
+                order[atomicAdd(st + 2, 1)] = i;
+                lev[i] = L;
+            }
         }
     }
 }
@@ -78,6 +84,7 @@ __global__ void k_advance(int* st) {
 void build_sched(Ctx& c, int n, const int* rp, const int* ci, int dir, Sched& out) {
     out.n = n;
     out.order.alloc(std::max(n, 1));
+    out.level.alloc(std::max(n, 1));
     out.nlev = 0;
     if (n == 0) return;
     auto nb = [](int64_t m) { return int(std::max<int64_t>(1, (m + 255) / 256)); };
@@ -96,7 +103,7 @@ void build_sched(Ctx& c, int n, const int* rp, const int* ci, int dir, Sched& ou
     c.sync();
     DBuf<int> dci(std::max(ndep, 1));
     k_dep_fill<<<nb(n), 256, 0, c.s>>>(rp, ci, n, dir, drp.p, fillc.p, dci.p);
-    k_zero_flag<<<nb(n), 256, 0, c.s>>>(indeg.p, n, flag.p);
+    k_zero_flag<<<nb(n), 256, 0, c.s>>>(indeg.p, n, flag.p, out.level.p);
     MG_CUDA(cudaMemsetAsync(pos.p, 0, sizeof(int), c.s));
     cub::DeviceScan::InclusiveSum(tmp.p, bytes, flag.p, pos.p + 1, n, c.s);
     k_compact<<<nb(n), 256, 0, c.s>>>(flag.p, pos.p, n, out.order.p);
@@ -110,7 +117,7 @@ void build_sched(Ctx& c, int n, const int* rp, const int* ci, int dir, Sched& ou
     int h[4] = {0, 0, 0, 0};
     for (;;) {
         for (int r = 0; r < 64; ++r) {
-            k_round<<<grid, 256, 0, c.s>>>(drp.p, dci.p, indeg.p, out.order.p, st.p);
+            k_round<<<grid, 256, 0, c.s>>>(drp.p, dci.p, indeg.p, out.order.p, st.p, out.level.p);
             k_advance<<<1, 1, 0, c.s>>>(st.p);
         }
         check_launch("sched rounds");
