@@ -34,14 +34,21 @@ typedef enum mprec_status {
     MPREC_CONFIG = 6,         /* ConfigError                                      */
     MPREC_INTERNAL = 7,
     MPREC_CUDA = 8,           /* CUDA runtime failure (no GPU, OOM, ...)           */
+    MPREC_IO = 9,             /* IoError (matrix_io.cpp, harness.cpp:153-188)      */
 } mprec_status;
 
 /* MethodSpec (proj/include/mprec/scaling.hpp:10-20); parse_method strings
- * "ilu0", "cpr-amg", "cptr3-amg" (scaling.cpp:5-15). */
+ * "ilu0", "cpr-amg", "cpr-direct", "cptr3-amg", "cptr-direct", "cptr3-direct"
+ * (scaling.cpp:5-15).  The -direct sub-solvers factor the sub-system densely
+ * (DenseFactor, dense_factor.cpp) and are meant for small grids (<= 20000
+ * sub-system rows). */
 typedef enum mprec_method {
     MPREC_METHOD_ILU0 = 0,
     MPREC_METHOD_CPR_AMG = 1,
+    MPREC_METHOD_CPR_DIRECT = 2,   /* dense LU of B_PP (small systems)           */
     MPREC_METHOD_CPTR3_AMG = 3,
+    MPREC_METHOD_CPTR_DIRECT = 4,  /* dense LU of the 2n_c B_ee (scaling.cpp:90) */
+    MPREC_METHOD_CPTR3_DIRECT = 5, /* dense LU of C_TT and B_PP                  */
 } mprec_method;
 
 /* AMGParams (proj/include/mprec/amg.hpp:12-16). */
@@ -132,6 +139,20 @@ int mprec_gpu_solve_dev(mprec_gpu_system* h, double tol, int max_iter, double* x
  * + solve + destroy. */
 int mprec_gpu_solve_system(const mprec_bsr* a, const double* b, int method, double tol,
                            int max_iter, double* x, mprec_solve_result* out);
+
+/* ingest_external (harness.cpp:153-188): Matrix Market "coordinate real
+ * general" + layout sidecar + rhs (matrix_io.cpp:40-121) read and assembled
+ * into a device BSR; every cell must carry P and T and (this path) the layout
+ * must be uniform.  The rhs is kept by the handle: mprec_gpu_setup(h, m, amg,
+ * NULL) uses it. */
+int mprec_gpu_ingest(const char* matrix_path, const char* layout_path, const char* rhs_path,
+                     mprec_gpu_system** out);
+int mprec_gpu_get_shape(mprec_gpu_system* h, int* n_cells, int* nb, int* nnzb);
+/* original A (BSR, column-major blocks) and the rhs the handle holds (either may be NULL) */
+int mprec_gpu_get_matrix(mprec_gpu_system* h, int* row_ptr, int* col_idx, double* values, double* b);
+/* write_block_matrix + write_vector (matrix_io.cpp:93-114), %.17g round-trip exact */
+int mprec_gpu_write_system(mprec_gpu_system* h, const char* matrix_path, const char* layout_path,
+                           const char* rhs_path);
 
 /* Parity diagnostics. */
 int mprec_gpu_get_scaled(mprec_gpu_system* h, double* abar_values, double* b_bar);

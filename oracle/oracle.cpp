@@ -215,6 +215,26 @@ Csr Bsr::extract_field(int local) const {
     return m;
 }
 
+// extract_submatrix({P,T},{P,T}) (block_matrix.cpp:142-170): rows/cols in cell
+// order then (P, T); every stored entry kept.
+static Csr extract_pt(const Bsr& a) {
+    const int P = a.nb - 2, T = a.nb - 1;
+    Csr m;
+    m.rows = m.cols = 2 * a.nc;
+    m.rp.assign(2 * a.nc + 1, 0);
+    for (int c = 0; c < a.nc; ++c)
+        for (int r = 0; r < 2; ++r) {
+            const int fr = r == 0 ? P : T;
+            for (int k = a.rp[c]; k < a.rp[c + 1]; ++k)
+                for (int q = 0; q < 2; ++q) {
+                    m.ci.push_back(2 * a.ci[k] + q);
+                    m.v.push_back(a.at(k, fr, q == 0 ? P : T));
+                }
+            m.rp[2 * c + r + 1] = int(m.ci.size());
+        }
+    return m;
+}
+
 // ================================================================ DenseLU ==
 // Eigen::PartialPivLU unblocked path (partial_lu_impl::unblocked_lu).
 void DenseLU::factor(const double* a, int n_) {
@@ -762,7 +782,14 @@ ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m) {
     if (m == Method::Ilu0) return s;
     std::vector<int> S;
     for (int k = 0; k < ns; ++k) S.push_back(k);
-    if (m == Method::Cpr) {
+    if (m == Method::CptrDirect) {  // scaling.cpp:90-105
+        const auto w = scaling_factors(a, {P, T}, S, "D_ss");
+        for (int c = 0; c < a.nc; ++c) combine_cell(s.a_bar, s.b_bar, c, {P, T}, S, w[c]);
+        s.scaling_record.push_back("D_es*D_ss^-1");
+        s.b_ee = extract_pt(s.a_bar);
+        return s;
+    }
+    if (m == Method::Cpr || m == Method::CprDirect) {
         std::vector<int> h = S;
         h.push_back(T);
         const auto w = scaling_factors(a, {P}, h, "D_hh");
@@ -771,7 +798,7 @@ ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m) {
         s.b_pp = s.a_bar.extract_field(P);
         return s;
     }
-    if (m == Method::Cptr3) {
+    if (m == Method::Cptr3 || m == Method::Cptr3Direct) {
         const auto w1 = scaling_factors(a, {P, T}, S, "D_ss");
         for (int c = 0; c < a.nc; ++c) combine_cell(s.a_bar, s.b_bar, c, {P, T}, S, w1[c]);
         s.scaling_record.push_back("[D_Ps;D_Ts]*D_ss^-1");
@@ -802,7 +829,7 @@ Vec Stage::apply(const Vec& r, const Ilu0Block& ilu) const {
     if (scope.empty()) return y;
     Vec sub(scope.size());
     for (size_t i = 0; i < scope.size(); ++i) sub[i] = r[scope[i]];
-    const Vec sol = amg->apply(sub);
+    const Vec sol = kind == AMG ? amg->apply(sub) : direct->solve(sub);
     for (size_t i = 0; i < scope.size(); ++i) y[scope[i]] = sol[i];
     return y;
 }
@@ -854,18 +881,33 @@ StagePreconditioner build_preconditioner(const ScaledSystem& sc, const AMGParams
     pc.method = sc.method;
     pc.a_bar = &sc.a_bar;
     const int nc = sc.a_bar.nc, nb = sc.a_bar.nb;
-    auto scoped = [&](const Csr& sub, int local) {
+    const bool direct = sc.method == Method::CprDirect || sc.method == Method::CptrDirect ||
+                        sc.method == Method::Cptr3Direct;
+    // make_scoped (stages.cpp:67-76)
+    auto scoped = [&](const Csr& sub, std::vector<int> scope) {
         Stage s;
-        s.kind = Stage::AMG;
-        s.scope = field_scope(nc, nb, local);
-        s.amg = std::make_shared<AMGHierarchy>(AMGHierarchy::setup(sub, p));
+        s.scope = std::move(scope);
+        if (direct) {
+            s.kind = Stage::DIRECT;
+            s.direct = std::make_shared<DenseFactor>(DenseFactor::factor(sub));
+        } else {
+            s.kind = Stage::AMG;
+            s.amg = std::make_shared<AMGHierarchy>(AMGHierarchy::setup(sub, p));
+        }
         return s;
     };
-    if (sc.method == Method::Cpr) {
-        pc.stages.push_back(scoped(sc.b_pp, nb - 2));
-    } else if (sc.method == Method::Cptr3) {
-        pc.stages.push_back(scoped(sc.c_tt, nb - 1));
-        pc.stages.push_back(scoped(sc.b_pp, nb - 2));
+    if (sc.method == Method::Cpr || sc.method == Method::CprDirect) {
+        pc.stages.push_back(scoped(sc.b_pp, field_scope(nc, nb, nb - 2)));
+    } else if (sc.method == Method::Cptr3 || sc.method == Method::Cptr3Direct) {
+        pc.stages.push_back(scoped(sc.c_tt, field_scope(nc, nb, nb - 1)));
+        pc.stages.push_back(scoped(sc.b_pp, field_scope(nc, nb, nb - 2)));
+    } else if (sc.method == Method::CptrDirect) {
+        std::vector<int> e;
+        for (int c = 0; c < nc; ++c) {
+            e.push_back(c * nb + nb - 2);
+            e.push_back(c * nb + nb - 1);
+        }
+        pc.stages.push_back(scoped(sc.b_ee, e));
     }
     pc.ilu = Ilu0Block::factor(sc.a_bar);
     Stage ilu;

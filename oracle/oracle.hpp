@@ -163,22 +163,24 @@ struct AMGHierarchy {
 };
 
 // ----- scaling + stages (scaling.cpp, stages.cpp) --------------------------
-enum class Method : int { Ilu0 = 0, Cpr = 1, Cptr3 = 3 };
+// method ids shared with include/mprec_gpu.h (scaling.hpp:10-20: Method x SubSolver)
+enum class Method : int { Ilu0 = 0, Cpr = 1, CprDirect = 2, Cptr3 = 3, CptrDirect = 4, Cptr3Direct = 5 };
 
 struct ScaledSystem {
     Bsr a_bar;
     Vec b_bar;
     Method method = Method::Ilu0;
-    Csr b_pp, c_tt;
+    Csr b_pp, c_tt, b_ee;  // b_ee: CPTR 2n_c x 2n_c (cell-interleaved P,T)
     std::vector<std::string> scaling_record;
 };
 
 ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m);  // scaling.cpp:149-158
 
 struct Stage {
-    enum Kind { AMG, ILU } kind = ILU;
+    enum Kind { AMG, DIRECT, ILU } kind = ILU;
     std::vector<int> scope;  // global indices (field_layout.cpp:110-125)
     std::shared_ptr<AMGHierarchy> amg;
+    std::shared_ptr<DenseFactor> direct;
     Vec apply(const Vec& r, const Ilu0Block& ilu) const;  // stages.cpp:25-34
 };
 

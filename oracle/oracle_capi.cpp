@@ -2,7 +2,9 @@
 // Same signatures as include/mprec_gpu.h with the prefix `orc_`, so the parity
 // tests drive both sides through one wrapper (tests/_native.py).
 #include <chrono>
+#include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 
 #include "../include/mprec_gpu.h"
@@ -62,6 +64,7 @@ double now_s() {
 struct orc_system {
     Bsr a;
     Vec b;
+    Vec b_ingested;
     ScaledSystem sc;
     StagePreconditioner prec;
     bool ready = false;
@@ -94,8 +97,11 @@ int orc_create(const mprec_bsr* a, orc_system** out) {
 
 int orc_setup(orc_system* h, int method, const mprec_amg_params* amg, const double* b) {
     return guard([&] {
-        if (method != MPREC_METHOD_ILU0 && method != MPREC_METHOD_CPR_AMG && method != MPREC_METHOD_CPTR3_AMG)
-            throw Error(CONFIG, "unknown method id " + std::to_string(method));
+        if (!b) {
+            if (int64_t(h->b_ingested.size()) != int64_t(h->a.dim())) throw Error(DIMENSION, "no rhs");
+            b = h->b_ingested.data();
+        }
+        if (method < 0 || method > 5) throw Error(CONFIG, "unknown method id " + std::to_string(method));
         h->ready = false;
         h->b.assign(b, b + h->a.dim());
         const double t0 = now_s();
@@ -199,13 +205,128 @@ int orc_stage_amg(orc_system* h, int stage, orc_amg** amg) {
     return guard([&] {
         if (!h->ready) throw Error(SETUP, "setup not done");
         if (stage < 0 || stage >= int(h->prec.stages.size()) || h->prec.stages[stage].kind != Stage::AMG)
-            throw Error(INDEX, "not an AMG stage");
+            throw Error(INDEX, "not an AMG stage");  // -direct stages have no hierarchy
         // non-owning view: the oracle AMG object lives in the preconditioner
         *amg = reinterpret_cast<orc_amg*>(h->prec.stages[stage].amg.get());
     });
 }
 
 void orc_destroy(orc_system* h) { delete h; }
+
+// read_matrix_market / read_layout / read_vector (matrix_io.cpp:40-121) +
+// BlockMatrix::from_scalar (block_matrix.cpp:71-94) + ingest_external checks
+// (harness.cpp:153-168); uniform layouts only (as the C ABI).
+int orc_ingest(const char* mtx, const char* layout, const char* rhs, orc_system** out) {
+    // C stdio, not iostreams: the oracle is loaded into Python processes whose
+    // numpy may have brought another libstdc++ (iostream locale clash).
+    return guard([&] {
+        auto io = [](const std::string& m) { return Error(9, m); };
+        struct F {
+            FILE* f;
+            explicit F(const char* p) : f(std::fopen(p, "r")) {}
+            ~F() {
+                if (f) std::fclose(f);
+            }
+        };
+        F lf(layout);
+        if (!lf.f) throw io(std::string("cannot open '") + layout + "' for reading");
+        int nu = 0, nc = 0;
+        if (std::fscanf(lf.f, "%d %d", &nu, &nc) != 2) throw io(std::string(layout) + ": bad layout header");
+        std::vector<int> cell(nu);
+        std::vector<char> tag(nu);
+        for (int g = 0; g < nu; ++g) {
+            char t[8];
+            if (std::fscanf(lf.f, "%d %7s", &cell[g], t) != 2) throw io(std::string(layout) + ": truncated layout");
+            tag[g] = t[0];
+        }
+        int nb = -1, g = 0;
+        for (int c = 0; c < nc; ++c) {
+            const int g0 = g;
+            while (g < nu && cell[g] == c && tag[g] == 's') ++g;
+            if (!(g < nu && cell[g] == c && tag[g] == 'P')) throw io("cell " + std::to_string(c) + " has no pressure unknown");
+            ++g;
+            if (!(g < nu && cell[g] == c && tag[g] == 'T'))
+                throw io("cell " + std::to_string(c) + " has no temperature unknown");
+            ++g;
+            if (nb < 0) nb = g - g0;
+            if (g - g0 != nb) throw Error(DIMENSION, "non-uniform layout");
+        }
+        if (g != nu || nc < 1) throw io(std::string(layout) + ": header cell count disagrees with tag list");
+        const int n = nc * nb;
+        F mf(mtx);
+        if (!mf.f) throw io(std::string("cannot open '") + mtx + "' for reading");
+        char line[4096];
+        if (!std::fgets(line, sizeof line, mf.f)) throw io(std::string(mtx) + ": empty file");
+        char w[5][64] = {};
+        if (std::sscanf(line, "%63s %63s %63s %63s %63s", w[0], w[1], w[2], w[3], w[4]) != 5 ||
+            std::strcmp(w[0], "%%MatrixMarket") || std::strcmp(w[1], "matrix") || std::strcmp(w[2], "coordinate") ||
+            std::strcmp(w[3], "real") || std::strcmp(w[4], "general"))
+            throw io(std::string(mtx) + ": expected 'matrix coordinate real general' header");
+        do {
+            if (!std::fgets(line, sizeof line, mf.f)) throw io(std::string(mtx) + ": bad size line");
+        } while (line[0] == '%' || line[0] == '\n');
+        int rows = 0, cols = 0, nnz = 0;
+        if (std::sscanf(line, "%d %d %d", &rows, &cols, &nnz) != 3) throw io(std::string(mtx) + ": bad size line");
+        if (rows != cols) throw io(std::string(mtx) + ": block matrix must be square");
+        if (rows != n) throw Error(DIMENSION, "scalar matrix does not match layout dimension");
+        std::vector<Triplet> t(nnz);
+        for (int k = 0; k < nnz; ++k) {
+            if (std::fscanf(mf.f, "%d %d %lf", &t[k].row, &t[k].col, &t[k].value) != 3)
+                throw io(std::string(mtx) + ": truncated entry list");
+            --t[k].row;
+            --t[k].col;
+        }
+        const Csr a = Csr::from_triplets(n, n, std::move(t));
+        std::map<std::pair<int, int>, Vec> blocks;
+        for (int c = 0; c < nc; ++c) blocks[{c, c}] = Vec(size_t(nb) * nb, 0.0);
+        for (int i = 0; i < n; ++i)
+            for (int k = a.rp[i]; k < a.rp[i + 1]; ++k) {
+                auto& blk = blocks[{i / nb, a.ci[k] / nb}];
+                if (blk.empty()) blk.assign(size_t(nb) * nb, 0.0);
+                blk[size_t(a.ci[k] % nb) * nb + i % nb] = a.v[k];
+            }
+        std::vector<int> rp(nc + 1, 0), ci;
+        Vec vals;
+        for (auto& kv : blocks) {
+            ci.push_back(kv.first.second);
+            vals.insert(vals.end(), kv.second.begin(), kv.second.end());
+            rp[kv.first.first + 1]++;
+        }
+        for (int c = 0; c < nc; ++c) rp[c + 1] += rp[c];
+        F rf(rhs);
+        if (!rf.f) throw io(std::string("cannot open '") + rhs + "' for reading");
+        Vec b;
+        double x;
+        while (std::fscanf(rf.f, "%lf", &x) == 1) b.push_back(x);
+        if (int(b.size()) != n)
+            throw io("rhs dimension " + std::to_string(b.size()) + " does not match matrix dimension " + std::to_string(n));
+        auto* h = new orc_system;
+        h->a = Bsr::create(nc, nb, rp.data(), ci.data(), vals.data());
+        h->b_ingested = std::move(b);
+        *out = h;
+    });
+}
+
+int orc_get_shape(orc_system* h, int* n_cells, int* nb, int* nnzb) {
+    return guard([&] {
+        if (n_cells) *n_cells = h->a.nc;
+        if (nb) *nb = h->a.nb;
+        if (nnzb) *nnzb = h->a.rp[h->a.nc];
+    });
+}
+
+int orc_get_matrix(orc_system* h, int* rp, int* ci, double* vals, double* b) {
+    return guard([&] {
+        if (rp) std::memcpy(rp, h->a.rp.data(), sizeof(int) * h->a.rp.size());
+        if (ci) std::memcpy(ci, h->a.ci.data(), sizeof(int) * h->a.ci.size());
+        if (vals) std::memcpy(vals, h->a.val.data(), sizeof(double) * h->a.val.size());
+        if (b) {
+            const Vec& src = h->b_ingested.empty() ? h->b : h->b_ingested;
+            if (int64_t(src.size()) != int64_t(h->a.dim())) throw Error(DIMENSION, "the handle holds no rhs");
+            std::memcpy(b, src.data(), sizeof(double) * src.size());
+        }
+    });
+}
 
 // ---- sub-solvers ----------------------------------------------------------
 

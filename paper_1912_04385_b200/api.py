@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 # ---- status codes / exceptions (errors.hpp:9-59) ---------------------------
-OK, DIMENSION, INDEX, SINGULAR_BLOCK, ZERO_PIVOT, SETUP, CONFIG, INTERNAL, CUDA = range(9)
+OK, DIMENSION, INDEX, SINGULAR_BLOCK, ZERO_PIVOT, SETUP, CONFIG, INTERNAL, CUDA, IO = range(10)
 
 
 class MprecError(RuntimeError):
@@ -66,12 +66,17 @@ class CudaError(MprecError):
     code = CUDA
 
 
+class IoError(MprecError):
+    code = IO
+
+
 _ERRORS = {c.code: c for c in (DimensionError, IndexError_, SingularBlockError, ZeroPivotError,
-                               SetupError, ConfigError, CudaError)}
+                               SetupError, ConfigError, CudaError, IoError)}
 
 # ---- methods (scaling.cpp:5-15) ---------------------------------------------
-METHOD_ILU0, METHOD_CPR_AMG, METHOD_CPTR3_AMG = 0, 1, 3
-_METHODS = {"ilu0": METHOD_ILU0, "cpr-amg": METHOD_CPR_AMG, "cptr3-amg": METHOD_CPTR3_AMG}
+METHOD_ILU0, METHOD_CPR_AMG, METHOD_CPR_DIRECT, METHOD_CPTR3_AMG, METHOD_CPTR_DIRECT, METHOD_CPTR3_DIRECT = range(6)
+_METHODS = {"ilu0": METHOD_ILU0, "cpr-amg": METHOD_CPR_AMG, "cpr-direct": METHOD_CPR_DIRECT,
+            "cptr3-amg": METHOD_CPTR3_AMG, "cptr-direct": METHOD_CPTR_DIRECT, "cptr3-direct": METHOD_CPTR3_DIRECT}
 
 
 def parse_method(name: str) -> int:
@@ -266,6 +271,10 @@ class Api:
             "reset_stats": (C.c_int, [vp]),
             "launch_count": (C.c_int, [vp, i64p]),
             "stream": (C.c_int, [vp, C.POINTER(vp)]),
+            "ingest": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(vp)]),
+            "get_shape": (C.c_int, [vp, ip, ip, ip]),
+            "get_matrix": (C.c_int, [vp, vp, vp, vp, vp]),
+            "write_system": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p]),
         }
         self.fn = {}
         for name, (res, args) in list(sig.items()) + list(optional.items()):
@@ -301,6 +310,21 @@ class Api:
 
     def ilu0(self, a) -> "ILU0Factor":
         return ILU0Factor(self, a.as_block() if isinstance(a, ScalarMatrix) else a)
+
+    def ingest(self, matrix_path: str, layout_path: str, rhs_path: str) -> "System":
+        """ingest_external (harness.cpp:153-188): Matrix Market + layout + rhs."""
+        h = C.c_void_p()
+        self.call("ingest", matrix_path.encode(), layout_path.encode(), rhs_path.encode(), C.byref(h))
+        nc, nb, nnzb = C.c_int(), C.c_int(), C.c_int()
+        self.call("get_shape", h, C.byref(nc), C.byref(nb), C.byref(nnzb))
+        rp = np.zeros(nc.value + 1, np.int32)
+        ci = np.zeros(nnzb.value, np.int32)
+        v = np.zeros(nnzb.value * nb.value * nb.value)
+        b = np.zeros(nc.value * nb.value)
+        self.call("get_matrix", h, _ptr(rp), _ptr(ci), _ptr(v), _ptr(b))
+        sysm = System.__new__(System)
+        sysm.api, sysm.a, sysm.h, sysm.method, sysm.b = self, BlockMatrix(nc.value, nb.value, rp, ci, v), h, None, b
+        return sysm
 
     def gmres(self, a, b, prec=None, tol=1e-8, max_iter=500) -> SolveResult:
         """gmres (gmres.cpp:8-106); a: BlockMatrix or ScalarMatrix; prec: None
@@ -352,8 +376,10 @@ class System:
         except Exception:
             pass
 
-    def setup(self, method, b, **amg) -> "System":
+    def setup(self, method, b=None, **amg) -> "System":
         m = parse_method(method) if isinstance(method, str) else int(method)
+        if b is None:  # rhs held by the handle (ingested system)
+            b = self.b
         self.b = _f64(b)
         if self.b.size != self.a.dim:
             raise DimensionError("rhs length mismatch")
@@ -361,6 +387,10 @@ class System:
         self.api.call("setup", self.h, m, C.byref(p) if p is not None else None, _ptr(self.b))
         self.method = m
         return self
+
+    def write(self, matrix_path: str, layout_path: str, rhs_path: str) -> None:
+        """write_block_matrix + write_vector (matrix_io.cpp:93-114); GPU library only."""
+        self.api.call("write_system", self.h, matrix_path.encode(), layout_path.encode(), rhs_path.encode())
 
     def apply(self, r) -> np.ndarray:
         r = _f64(r)

@@ -236,6 +236,24 @@ __global__ void k_combine(double* y, const double* w, const double* xs, int fx, 
     }
 }
 
+__global__ void k_add2(double* y, const double* a, const double* b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = a[i] + b[i];
+}
+
+__global__ void k_gather_pt(double* out, const double* x, int nc, int nb) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < 2 * nc) out[t] = x[(int64_t)(t >> 1) * nb + nb - 2 + (t & 1)];
+}
+
+__global__ void k_scatter_pt(double* y, const double* sub, int nc, int nb) {
+    const int64_t n = (int64_t)nc * nb;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = int(i / nb), f = int(i - (int64_t)c * nb);
+        y[i] = f >= nb - 2 ? sub[2 * c + (f - (nb - 2))] : 0.0;
+    }
+}
+
 inline int red_grid(int64_t n) {
     int64_t g = (n + kRT - 1) / kRT;
     return int(std::max<int64_t>(1, std::min<int64_t>(g, kRedBlocks)));
@@ -325,4 +343,23 @@ void stage_combine(Ctx& c, double* y, const double* w, const double* xs, int fx,
     check_launch("combine");
 }
 
+}  // namespace mg
+
+namespace mg {
+void add2(Ctx& c, double* y, const double* a, const double* b, int64_t n) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 24.0 * n);
+    k_add2<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(y, a, b, n);
+    check_launch("add2");
+}
+void gather_pt(Ctx& c, double* out, const double* x, int nc, int nb) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 32.0 * nc);
+    k_gather_pt<<<(2 * nc + 255) / 256, 256, 0, c.s>>>(out, x, nc, nb);
+    check_launch("gather_pt");
+}
+void scatter_pt(Ctx& c, double* y, const double* sub, int nc, int nb) {
+    const int64_t n = (int64_t)nc * nb;
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * n + 16.0 * nc);
+    k_scatter_pt<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(y, sub, nc, nb);
+    check_launch("scatter_pt");
+}
 }  // namespace mg

@@ -256,7 +256,13 @@ void fill_result(mprec_solve_result* r, const GmresOut& g, int attempts, double 
 
 }  // namespace
 
+static bool is_cptr3_method(int m) { return m == MPREC_METHOD_CPTR3_AMG || m == MPREC_METHOD_CPTR3_DIRECT; }
+
 namespace mg {
+void ingest(Ctx& c, const char* mtx, const char* layout, const char* rhs, Pattern& pat, DBuf<double>& val, int* n_cells,
+            int* nb_out, std::vector<double>& b);
+void write_system(const char* mtx, const char* layout, const char* rhs, int nc, int nb, const std::vector<int>& rp,
+                  const std::vector<int>& ci, const std::vector<double>& val, const double* b);
 void ilu_timeline(Ctx& c, Ilu& ilu, const double* r, double* y, long long* ts_dev, int blocks);
 void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int* nl_f, int* nl_b);
 void gs_band_timeline(Ctx& c, Amg& amg, int l, long long* host_ts, int* nbands);
@@ -287,7 +293,9 @@ struct mprec_gpu_system {
     int nb = 0;
     int64_t n = 0;
     DBuf<double> a_val, abar_val, lu_val, b, bbar, fP, fT;
-    std::unique_ptr<Amg> amgT, amgP;
+    std::unique_ptr<Amg> amgT, amgP, amgE;  // amgE: CPTR's dense B_ee solve
+    DCsr b_ee;
+    DBuf<double> gE, xE;
     Ilu ilu;
     int method = -1;
     bool ready = false;
@@ -296,11 +304,16 @@ struct mprec_gpu_system {
     DBuf<double> gT, xT, gP, vP, z, u, w, x, r, y;
     Krylov kr;
     std::vector<std::unique_ptr<mprec_gpu_amg>> views;
+    std::vector<double> b_host;  // rhs kept by mprec_gpu_ingest / the last setup
 
     BsrView A() { return view_of(pat, nb, a_val.p); }
     BsrView Abar() { return view_of(pat, nb, abar_val.p); }
     int P() const { return nb - 2; }
     int T() const { return nb - 1; }
+
+    static bool is_cpr(int m) { return m == MPREC_METHOD_CPR_AMG || m == MPREC_METHOD_CPR_DIRECT; }
+    static bool is_cptr3(int m) { return m == MPREC_METHOD_CPTR3_AMG || m == MPREC_METHOD_CPTR3_DIRECT; }
+    int n_stages() const { return method == MPREC_METHOD_ILU0 ? 1 : (is_cptr3(method) ? 3 : 2); }
 
     // StagePreconditioner::apply (stages.cpp:36-59), device pointers
     void prec_apply(const double* rin, double* yout) {
@@ -308,7 +321,15 @@ struct mprec_gpu_system {
         const int nc = pat.nc;
         if (method == MPREC_METHOD_ILU0) {
             ilu.apply(c, rin, yout);
-        } else if (method == MPREC_METHOD_CPR_AMG) {
+        } else if (method == MPREC_METHOD_CPTR_DIRECT) {
+            // x = M1 r (B_ee scope); z = r - A x; y = x + M2 z
+            gather_pt(c, gE.p, rin, nc, nb);
+            amgE->apply(c, gE.p, xE.p);
+            scatter_pt(c, x.p, xE.p, nc, nb);
+            bsr_spmv(c, Abar(), x.p, z.p, rin, MPREC_K_SPMV);
+            ilu.apply(c, z.p, w.p);
+            add2(c, yout, x.p, w.p, n);  // y = x + M2 z (stages.cpp:48)
+        } else if (is_cpr(method)) {
             gather_stride(c, gP.p, rin, nc, nb, P());
             amgP->apply(c, gP.p, vP.p);
             bsr_col_update(c, Abar(), P(), vP.p, rin, z.p, nullptr, 0);
@@ -329,15 +350,21 @@ struct mprec_gpu_system {
     void stage_apply(int i, const double* rin, double* yout) {
         Ctx& c = ctx;
         const int nc = pat.nc;
-        const int nst = method == MPREC_METHOD_CPTR3_AMG ? 3 : (method == MPREC_METHOD_CPR_AMG ? 2 : 1);
+        const int nst = n_stages();
         if (i < 0 || i >= nst) throw Error(MPREC_INDEX, "stage out of range");
         if (i == nst - 1) {
             ilu.apply(c, rin, yout);
             return;
         }
+        if (method == MPREC_METHOD_CPTR_DIRECT) {
+            gather_pt(c, gE.p, rin, nc, nb);
+            amgE->apply(c, gE.p, xE.p);
+            scatter_pt(c, yout, xE.p, nc, nb);
+            return;
+        }
         Amg* a = nullptr;
         int f = 0;
-        if (method == MPREC_METHOD_CPR_AMG) {
+        if (is_cpr(method)) {
             a = amgP.get();
             f = P();
         } else if (i == 0) {
@@ -435,7 +462,7 @@ int mprec_gpu_create(const mprec_bsr* a, mprec_gpu_system** out) {
 int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg, const double* b) {
     return guard([&] {
         if (!h) throw Error(MPREC_DIMENSION, "null handle");
-        if (method != MPREC_METHOD_ILU0 && method != MPREC_METHOD_CPR_AMG && method != MPREC_METHOD_CPTR3_AMG)
+        if (method < MPREC_METHOD_ILU0 || method > MPREC_METHOD_CPTR3_DIRECT)
             throw Error(MPREC_CONFIG, "unknown method id " + std::to_string(method));
         if (method != MPREC_METHOD_ILU0 && h->nb < 2)
             throw Error(MPREC_DIMENSION, "CPR/CPTR3 need P and T unknowns (nb >= 2)");
@@ -444,6 +471,12 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
         const double t0 = now_s();
         const int64_t n = h->n;
         const size_t nv = size_t(h->pat.nnzb) * h->nb * h->nb;
+        if (!b) {
+            if (int64_t(h->b_host.size()) != n) throw Error(MPREC_DIMENSION, "no rhs: pass b or ingest one");
+            b = h->b_host.data();
+        } else {
+            h->b_host.assign(b, b + n);
+        }
         h->b.upload(b, n, c.s);
         h->bbar.ensure(n);
         copy(c, h->bbar.p, h->b.p, n);
@@ -465,7 +498,31 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
         h->views.clear();
         h->amgT.reset();
         h->amgP.reset();
-        if (method == MPREC_METHOD_CPTR3_AMG) {
+        h->amgE.reset();
+        // -direct: the stage sub-system is factored densely (a single-level hierarchy
+        // whose coarsest solve is the whole sub-system, DenseFactor in make_scoped)
+        const bool direct = method == MPREC_METHOD_CPR_DIRECT || method == MPREC_METHOD_CPTR_DIRECT ||
+                            method == MPREC_METHOD_CPTR3_DIRECT;
+        if (direct) {
+            prm.max_coarse = 0x7fffffff;
+            prm.max_levels = 1;
+        }
+        if (method == MPREC_METHOD_CPTR_DIRECT) {
+            DCsr& e = h->b_ee;
+            e.n = e.m = 2 * nc;
+            e.nnz = 4 * h->pat.nnzb;
+            e.rp.alloc(2 * nc + 1);
+            e.ci.alloc(e.nnz);
+            e.v.alloc(e.nnz);
+            extract_pt(c, h->Abar(), e.rp.p, e.ci.p, e.v.p);
+            h->amgE = std::make_unique<Amg>();
+            CsrView ev = e.view();
+            ev.diag = nullptr;
+            h->amgE->setup(c, ev, prm);
+            h->gE.ensure(2 * nc);
+            h->xE.ensure(2 * nc);
+        }
+        if (is_cptr3_method(method)) {
             h->fT.ensure(h->pat.nnzb);
             extract_field(c, h->Abar(), h->T(), h->fT.p);
             CsrView a0{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fT.p, h->pat.dpos.p};
@@ -473,7 +530,7 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
             Trace tr(&c, "AMG(C_TT) setup total");
             h->amgT->setup(c, a0, prm, &h->pat);
         }
-        if (method != MPREC_METHOD_ILU0) {
+        if (method == MPREC_METHOD_CPR_AMG || method == MPREC_METHOD_CPR_DIRECT || is_cptr3_method(method)) {
             h->fP.ensure(h->pat.nnzb);
             extract_field(c, h->Abar(), h->P(), h->fP.p);
             CsrView a0{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fP.p, h->pat.dpos.p};
@@ -496,6 +553,50 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
         h->method = method;
         h->ready = true;
         h->setup_s = now_s() - t0;
+    });
+}
+
+int mprec_gpu_ingest(const char* mtx, const char* layout, const char* rhs, mprec_gpu_system** out) {
+    return guard([&] {
+        if (!mtx || !layout || !rhs || !out) throw Error(MPREC_DIMENSION, "null argument");
+        auto h = std::make_unique<mprec_gpu_system>();
+        int nc = 0, nb = 0;
+        ingest(h->ctx, mtx, layout, rhs, h->pat, h->a_val, &nc, &nb, h->b_host);
+        h->nb = nb;
+        h->n = int64_t(nc) * nb;
+        *out = h.release();
+    });
+}
+
+int mprec_gpu_get_shape(mprec_gpu_system* h, int* n_cells, int* nb, int* nnzb) {
+    return guard([&] {
+        if (!h) throw Error(MPREC_DIMENSION, "null handle");
+        if (n_cells) *n_cells = h->pat.nc;
+        if (nb) *nb = h->nb;
+        if (nnzb) *nnzb = h->pat.nnzb;
+    });
+}
+
+int mprec_gpu_get_matrix(mprec_gpu_system* h, int* rp, int* ci, double* vals, double* b) {
+    return guard([&] {
+        if (!h) throw Error(MPREC_DIMENSION, "null handle");
+        if (rp) std::memcpy(rp, h->pat.h_rp.data(), sizeof(int) * h->pat.h_rp.size());
+        if (ci) std::memcpy(ci, h->pat.h_ci.data(), sizeof(int) * h->pat.h_ci.size());
+        if (vals) h->a_val.download(vals, size_t(h->pat.nnzb) * h->nb * h->nb, h->ctx.s);
+        if (b) {
+            if (int64_t(h->b_host.size()) != h->n) throw Error(MPREC_DIMENSION, "the handle holds no rhs");
+            std::memcpy(b, h->b_host.data(), sizeof(double) * h->n);
+        }
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_write_system(mprec_gpu_system* h, const char* mtx, const char* layout, const char* rhs) {
+    return guard([&] {
+        if (!h || !mtx || !layout) throw Error(MPREC_DIMENSION, "null argument");
+        const std::vector<double> v = h->a_val.to_host(h->ctx.s, size_t(h->pat.nnzb) * h->nb * h->nb);
+        write_system(mtx, layout, rhs, h->pat.nc, h->nb, h->pat.h_rp, h->pat.h_ci, v,
+                     int64_t(h->b_host.size()) == h->n ? h->b_host.data() : nullptr);
     });
 }
 
@@ -593,14 +694,14 @@ int mprec_gpu_get_ilu(mprec_gpu_system* h, double* lu) {
 int mprec_gpu_n_stages(mprec_gpu_system* h, int* n) {
     return guard([&] {
         if (!h) throw Error(MPREC_DIMENSION, "null handle");
-        *n = !h->ready ? 0 : (h->method == MPREC_METHOD_CPTR3_AMG ? 3 : (h->method == MPREC_METHOD_CPR_AMG ? 2 : 1));
+        *n = !h->ready ? 0 : h->n_stages();
     });
 }
 
 int mprec_gpu_stage_amg(mprec_gpu_system* h, int stage, mprec_gpu_amg** out) {
     return guard([&] {
         if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
-        Amg* a = nullptr;
+        Amg* a = nullptr;  // -direct stages have no hierarchy (as in the oracle)
         if (h->method == MPREC_METHOD_CPR_AMG && stage == 0) a = h->amgP.get();
         if (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) a = h->amgT.get();
         if (h->method == MPREC_METHOD_CPTR3_AMG && stage == 1) a = h->amgP.get();
@@ -827,7 +928,7 @@ int mprec_gpu_debug_gs(mprec_gpu_system* h, int stage, int level, int reps, doub
     return guard([&] {
         if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
         Amg* a = (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) ? h->amgT.get() : h->amgP.get();
-        if (level < 0 || level + 1 >= a->n_levels()) throw Error(MPREC_INDEX, "level out of range");
+        if (!a || level < 0 || level + 1 >= a->n_levels()) throw Error(MPREC_INDEX, "level out of range");
         gs_bench(h->ctx, *a, level, reps, ms_f, ms_b, nl_f, nl_b);
         if (level == 0 && *nl_f >= 0) {
             *nl_f = h->pat.fwd.nlev;

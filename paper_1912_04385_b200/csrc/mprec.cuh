@@ -93,6 +93,10 @@ void gather_stride(Ctx& c, double* out, const double* x, int nc, int stride, int
 // vs on field fv; either may be null)
 void stage_combine(Ctx& c, double* y, const double* w, const double* xs, int fx, const double* vs, int fv,
                    int nc, int nb);
+// two-field (P,T) gather / zero-padded scatter of cell-interleaved sub-vectors (CPTR scope)
+void gather_pt(Ctx& c, double* out, const double* x, int nc, int nb);
+void add2(Ctx& c, double* y, const double* a, const double* b, int64_t n);  // y = a + b
+void scatter_pt(Ctx& c, double* y, const double* sub, int nc, int nb);
 
 // ---- bsr.cu ------------------------------------------------------------------
 // y = A x  or  y = b - A x  (b != nullptr); flat (scalar-CSR) semantics
@@ -108,6 +112,8 @@ void bsr_col_update(Ctx& c, const BsrView& a, int f, const double* xs, const dou
 void left_scale(Ctx& c, const BsrView& abar, double* bbar, int method);
 // vals[k] = A_k(f, f)  (extract_submatrix on a single field, pattern = block pattern)
 void extract_field(Ctx& c, const BsrView& a, int f, double* vals);
+// B_ee (CPTR): CSR with 2 n_c rows, cell-interleaved (P, T); erp[2nc+1], eci/ev[4 nnzb]
+void extract_pt(Ctx& c, const BsrView& a, int* erp, int* eci, double* ev);
 
 // ---- ilu.cu ------------------------------------------------------------------
 struct Ilu {

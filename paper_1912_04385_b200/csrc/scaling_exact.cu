@@ -127,7 +127,8 @@ __global__ void k_scale_cpr(const int* rp, const int* dpos, double* val, double*
 
 // CPTR3 (scaling.cpp:107-147): e = {P,T} rows -= (D_es D_ss^-1) * s rows, then
 // T rows -= (D_Tp * (1/D_PP)) * P rows on the once-scaled block row.
-__global__ void k_scale_cptr3(const int* rp, const int* dpos, double* val, double* b, int nc, int nb, int* err) {
+__global__ void k_scale_cptr3(const int* rp, const int* dpos, double* val, double* b, int nc, int nb, int* err,
+                              int second) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nc) return;
     const int ns = nb - 2, P = nb - 2, T = nb - 1;
@@ -145,6 +146,7 @@ __global__ void k_scale_cptr3(const int* rp, const int* dpos, double* val, doubl
         scaling_w(d, nb, tl, 2, sl, ns, inv, w);
         combine_cell(rp, val, b, c, nb, tl, 2, sl, ns, w);
     }
+    if (!second) return;  // CPTR (scaling.cpp:90-105): first scaling only
     const double pp = d[P * nb + P];
     // inverted_copy of the 1x1 block: tol = 1e-12|pp| -> fails iff |pp| <= tol
     if (fabs(pp) <= 1e-12 * fabs(pp)) {
@@ -161,7 +163,32 @@ __global__ void k_extract(const double* val, int nnzb, int nb, int f, double* ou
     if (k < nnzb) out[k] = val[((int64_t)k * nb + f) * nb + f];
 }
 
+// extract_submatrix({P,T},{P,T}) as CSR (2 n_c rows, cell-interleaved P,T)
+__global__ void k_extract_pt(const int* rp, const int* ci, const double* val, int nc, int nb, int* erp, int* eci,
+                             double* ev) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * nc) return;
+    const int c = t >> 1, r = t & 1;
+    const int P = nb - 2, fr = r ? nb - 1 : P;
+    const int nblk = rp[c + 1] - rp[c];
+    int o = 4 * rp[c] + r * 2 * nblk;
+    erp[t] = o;
+    if (t == 2 * nc - 1) erp[2 * nc] = 4 * rp[nc];
+    for (int k = rp[c]; k < rp[c + 1]; ++k)
+        for (int q = 0; q < 2; ++q) {
+            eci[o] = 2 * ci[k] + q;
+            ev[o] = val[((int64_t)k * nb + (q ? nb - 1 : P)) * nb + fr];
+            ++o;
+        }
+}
+
 }  // namespace
+
+void extract_pt(Ctx& c, const BsrView& a, int* erp, int* eci, double* ev) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 40.0 * a.nnzb);
+    k_extract_pt<<<(2 * a.nc + 255) / 256, 256, 0, c.s>>>(a.rp, a.ci, a.val, a.nc, a.nb, erp, eci, ev);
+    check_launch("extract_pt");
+}
 
 void left_scale(Ctx& c, const BsrView& a, double* bbar, int method) {
     if (method == MPREC_METHOD_ILU0) return;
@@ -173,10 +200,12 @@ void left_scale(Ctx& c, const BsrView& a, double* bbar, int method) {
     {
         Ctx::Scope sc(&c, MPREC_K_BLAS1, 2.0 * a.nnzb * 8.0 * a.nb * a.nb);
         const int th = 128, g = (a.nc + th - 1) / th;
-        if (method == MPREC_METHOD_CPR_AMG)
+        if (method == MPREC_METHOD_CPR_AMG || method == MPREC_METHOD_CPR_DIRECT)
             k_scale_cpr<<<g, th, 0, c.s>>>(a.rp, a.dpos, a.val, bbar, a.nc, a.nb, c.err.p);
-        else if (method == MPREC_METHOD_CPTR3_AMG)
-            k_scale_cptr3<<<g, th, 0, c.s>>>(a.rp, a.dpos, a.val, bbar, a.nc, a.nb, c.err.p);
+        else if (method == MPREC_METHOD_CPTR3_AMG || method == MPREC_METHOD_CPTR3_DIRECT ||
+                 method == MPREC_METHOD_CPTR_DIRECT)
+            k_scale_cptr3<<<g, th, 0, c.s>>>(a.rp, a.dpos, a.val, bbar, a.nc, a.nb, c.err.p,
+                                             method != MPREC_METHOD_CPTR_DIRECT);
         else
             throw Error(MPREC_CONFIG, "unknown method id " + std::to_string(method));
         check_launch("left_scale");
@@ -184,7 +213,7 @@ void left_scale(Ctx& c, const BsrView& a, double* bbar, int method) {
     MG_CUDA(cudaMemcpyAsync(h_err, c.err.p, sizeof(h_err), cudaMemcpyDeviceToHost, c.s));
     c.sync();
     if (h_err[0] != big) {
-        const char* what = method == MPREC_METHOD_CPR_AMG ? "D_hh" : "D_ss";
+        const char* what = (method == MPREC_METHOD_CPR_AMG || method == MPREC_METHOD_CPR_DIRECT) ? "D_hh" : "D_ss";
         throw Error(MPREC_SINGULAR_BLOCK, std::string("singular ") + what + " block in cell " + std::to_string(h_err[0]),
                     h_err[0]);
     }

@@ -82,6 +82,21 @@ def test_solve_parity(gpu, orc, name, method):
     assert rel(rg.x, ro.x) < 1e-6
 
 
+@pytest.mark.parametrize("method", ["cpr-direct", "cptr-direct", "cptr3-direct"])
+def test_direct_methods_parity(gpu, orc, method):
+    a, b, xs = small_system("g12x10_nb4_band")
+    sg, so = _pair(gpu, orc, a, b, method)
+    ag, bg = sg.scaled()
+    ao, bo = so.scaled()
+    assert np.array_equal(ag, ao) and np.array_equal(bg, bo)
+    assert np.array_equal(sg.ilu_values(), so.ilu_values())
+    r = random_vec(a.dim, 5)
+    assert rel(sg.apply(r), so.apply(r)) < APPLY_TOL
+    rg, ro = sg.solve(), so.solve()
+    assert abs(rg.iterations - ro.iterations) <= 1 and rg.converged == ro.converged
+    assert rel(rg.x, ro.x) < 1e-6
+
+
 @pytest.mark.parametrize("cid", [1, 2, 3])
 def test_baseline_configs_small(gpu, orc, cid):
     """BASELINE.json configs 1-3 at full size: setup bitwise, iterations +-1."""

@@ -285,7 +285,7 @@ def test_acceptance_7_amg_scalability(api):
 # test_stages.cpp:93-272
 
 def test_method_names():
-    for name in ("ilu0", "cpr-amg", "cptr3-amg"):
+    for name in ("ilu0", "cpr-direct", "cpr-amg", "cptr-direct", "cptr3-direct", "cptr3-amg"):
         assert method_name(parse_method(name)) == name
     with pytest.raises(ConfigError):
         parse_method("cptr-amg")
@@ -359,7 +359,7 @@ def _densify(n, op):
     return np.column_stack([op(np.eye(n)[:, j]) for j in range(n)])
 
 
-@pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
+@pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg", "cpr-direct", "cptr-direct", "cptr3-direct"])
 def test_stage_composition_equals_explicit(api, method):
     """Alg. 1/2 == M1 + M2(I - A M1) [+ M3(I - A M2)(I - A M1)]."""
     a = random_block_system(4, 2, 11)
@@ -394,7 +394,7 @@ def test_stage_counts_and_scopes(api):
     assert np.all(y0[~mask_t] == 0) and np.all(y1[~mask_p] == 0)
 
 
-@pytest.mark.parametrize("method", ["ilu0", "cpr-amg", "cptr3-amg"])
+@pytest.mark.parametrize("method", ["ilu0", "cpr-direct", "cptr-direct", "cptr3-direct", "cptr3-amg"])
 def test_preconditioners_linear_and_zero(api, method):
     a = random_block_system(3, 3, 29)
     s = api.system(a).setup(method, random_vec(a.dim, 1))
@@ -428,3 +428,72 @@ def test_solve_system_recovers_xstar(api, method):
     r = api.system(a).setup(method, b).solve()
     assert r.converged and r.final_true_residual <= 1e-8
     assert np.linalg.norm(r.x - xs) / np.linalg.norm(xs) < 1e-6
+
+
+def test_cptr_scaling_matches_dense_oracle(api):
+    """test_stages.cpp:152-162 (B_ee is the elliptic view of the scaled system)."""
+    a = random_block_system(4, 3, 5)
+    b = random_vec(a.dim, 6)
+    s = api.system(a).setup("cptr-direct", b)
+    abar, bbar = s.scaled()
+    e = _scaling_oracle(a, "cptr")
+    want = e @ a.to_dense()
+    got = BlockMatrix(a.n_cells, a.nb, a.row_ptr, a.col_idx, abar).to_dense()
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-13
+    assert np.linalg.norm(bbar - e @ b) / np.linalg.norm(b) < 1e-13
+    assert s.n_stages() == 2
+    r = random_vec(a.dim, 7)
+    y0 = s.apply_stage(0, r)
+    mask = np.zeros(a.dim, bool)
+    mask[a.nb - 2::a.nb] = True
+    mask[a.nb - 1::a.nb] = True
+    assert np.all(y0[~mask] == 0)  # scope = indices_of(elliptic)
+
+
+@pytest.mark.parametrize("method", ["cpr-direct", "cptr-direct", "cptr3-direct"])
+def test_preconditioned_solution_matches_unscaled(api, method):
+    """test_krylov.cpp:119-139: direct methods, tol 1e-12, x vs the dense solve."""
+    a = random_block_system(5, 3, 23)
+    b = random_vec(a.dim, 24)
+    x_ref = np.linalg.solve(a.to_dense(), b)
+    r = api.system(a).setup(method, b).solve(tol=1e-12, max_iter=200)
+    assert r.converged
+    assert np.linalg.norm(r.x - x_ref) / np.linalg.norm(x_ref) < 1e-8
+
+
+def test_acceptance_5_direct_methods_exact_on_decoupled_fields(api):
+    """acceptance.cpp:193-226: fields mutually decoupled, tridiagonal chains per
+    field -> every -direct method converges in exactly one iteration."""
+    rng = np.random.default_rng(505)
+    n_cells, blocks = 20, {}
+    for c in range(n_cells):
+        blocks[(c, c)] = np.diag(3.0 + rng.uniform(0.1, 0.9, 3))
+        if c + 1 < n_cells:
+            blocks[(c, c + 1)] = np.diag(-rng.uniform(0.1, 0.9, 3))
+            blocks[(c + 1, c)] = np.diag(-rng.uniform(0.1, 0.9, 3))
+    a = BlockMatrix.from_dense_blocks(n_cells, 3, blocks)
+    b = random_vec(a.dim, 42)
+    for method in ("cpr-direct", "cptr-direct", "cptr3-direct"):
+        r = api.system(a).setup(method, b).solve()
+        assert r.converged and r.iterations == 1, (method, r.iterations)
+
+
+def test_acceptance_3_compositions_on_random_systems(api):
+    """acceptance.cpp:120-167 (10 systems here): staged applications equal the
+    explicit compositions with -direct sub-solvers."""
+    worst = 0.0
+    for trial in range(10):
+        a = random_block_system(2 + trial % 7, 3, 700 + trial)
+        n = a.dim
+        r = random_vec(n, 800 + trial)
+        for method in ("cpr-direct", "cptr3-direct"):
+            s = api.system(a).setup(method, random_vec(n, 1))
+            abar = BlockMatrix(a.n_cells, a.nb, a.row_ptr, a.col_idx, s.scaled()[0]).to_dense()
+            ms = [_densify(n, lambda v, i=i: s.apply_stage(i, v)) for i in range(s.n_stages())]
+            eye = np.eye(n)
+            if len(ms) == 2:
+                comp = (ms[0] + ms[1] @ (eye - abar @ ms[0])) @ r
+            else:
+                comp = (ms[0] + ms[1] @ (eye - abar @ ms[0]) + ms[2] @ (eye - abar @ ms[1]) @ (eye - abar @ ms[0])) @ r
+            worst = max(worst, np.linalg.norm(s.apply(r) - comp) / (1.0 + np.linalg.norm(comp)))
+    assert worst <= 1e-13, worst
