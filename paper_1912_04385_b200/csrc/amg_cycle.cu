@@ -9,6 +9,7 @@
 // order from an atomic counter, the new iterate is written to a fresh buffer
 // pre-filled with the kPending sentinel and consumers poll the producer's value
 // (double buffering also makes the "old" reads race-free for any pattern).
+#include <cub/cub.cuh>
 #include <cstdlib>
 
 #include "mprec.cuh"
@@ -76,6 +77,94 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp
     }
 }
 
+// CTA per band of B consecutive rows (doacross).  The band's new
+// iterate lives in shared memory (kPending sentinel), so dependencies inside
+// the band are resolved by an on-SM poll instead of an L2 round trip; rows of
+// the band are claimed by the CTA's warps in global DAG-level order (`border`)
+// and bands are claimed in sweep order, hence deadlock-free.  Row arithmetic
+// is identical to k_gs (warp per row).
+// CTA per band of B consecutive rows (doacross).  The band's new
+// iterate lives in shared memory (kPending sentinel), so dependencies inside
+// the band are resolved by an on-SM poll instead of an L2 round trip; rows of
+// the band are claimed by the CTA's warps in global DAG-level order (`border`)
+// and bands are claimed in sweep order, hence deadlock-free.  Row arithmetic
+// is identical to k_gs (warp per row).  Chosen per AMG level by a setup-time
+// measurement (Amg::setup) against the row-per-warp sweep.
+template <int DIR>
+__global__ void __launch_bounds__(1024) k_gs_cta(const int* __restrict__ rp, const int* __restrict__ ci,
+                                                 const double* __restrict__ v, const double* __restrict__ invd,
+                                                 const double* __restrict__ b, const double* __restrict__ xold,
+                                                 double* xnew, const int* __restrict__ border, int n, int B,
+                                                 int nbands, int* counter) {
+    extern __shared__ double xs[];
+    __shared__ int band_sh, claim_sh;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int t = atomicAdd(counter, 1);
+            band_sh = DIR > 0 ? t : nbands - 1 - t;
+            claim_sh = 0;
+            if (t >= nbands) band_sh = -1;
+        }
+        __syncthreads();
+        const int band = band_sh;
+        if (band < 0) return;
+        const int b0 = band * B, b1 = min(n, b0 + B), nrow = b1 - b0;
+        for (int q = threadIdx.x; q < nrow; q += blockDim.x)
+            reinterpret_cast<unsigned long long*>(xs)[q] = kPending;
+        __syncthreads();
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(&claim_sh, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= nrow) break;
+            const int i = __ldg(border + b0 + t);
+            const int k0 = __ldg(rp + i), k1 = __ldg(rp + i + 1);
+            const double bi = __ldg(b + i), dii = __ldg(invd + i);
+            double acc = 0.0;
+            for (int base = k0; base < k1; base += 32) {
+                const int k = base + lane;
+                const bool valid = k < k1;
+                const int j = valid ? __ldg(ci + k) : i;
+                const bool off = valid && j != i;
+                const double a = off ? __ldg(v + k) : 0.0;
+                const bool dep = off && (DIR > 0 ? (j < i) : (j > i));
+                const bool local = dep && j >= b0 && j < b1;
+                double xj = 0.0;
+                if (off && !dep && xold) xj = __ldg(xold + j);
+                unsigned long long raw = 0;
+                if (dep && !local) raw = ld_relaxed(xnew + j);
+                if (local) raw = reinterpret_cast<volatile unsigned long long*>(xs)[j - b0];
+                bool pend = dep && raw == kPending;
+                while (__any_sync(0xffffffffu, pend)) {
+                    if (pend) {
+                        raw = local ? reinterpret_cast<volatile unsigned long long*>(xs)[j - b0] : ld_relaxed(xnew + j);
+                        pend = raw == kPending;
+                    }
+                }
+                if (dep) xj = __longlong_as_double((long long)raw);
+                acc += a * xj;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) {
+                const double xi = (bi - acc) * dii;
+                reinterpret_cast<volatile double*>(xs)[i - b0] = xi;
+                st_pub(xnew + i, xi);
+            }
+        }
+    }
+}
+
+__global__ void k_band_key(const int* lev, int n, int B, unsigned long long* key, int* row) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        key[i] = ((unsigned long long)(i / B) << 32) | (unsigned)lev[i];
+        row[i] = i;
+    }
+}
+
 __global__ void k_invd(const double* v, const int* diag, int n, double* invd) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) invd[i] = 1.0 / v[diag[i]];
@@ -136,6 +225,48 @@ void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, dou
     check_launch("gs_sweep");
 }
 
+// rows of every band of B rows in global DAG-level order
+void build_band_order(Ctx& c, int n, const int* lev, int B, DBuf<int>& border) {
+    DBuf<unsigned long long> key(n), skey(n);
+    DBuf<int> row(n);
+    border.alloc(std::max(n, 1));
+    k_band_key<<<(n + 255) / 256, 256, 0, c.s>>>(lev, n, B, key.p, row.p);
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, skey.p, row.p, border.p, n, 0, 64, c.s);
+    DBuf<char> tmp(bytes + 16);
+    cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, skey.p, row.p, border.p, n, 0, 64, c.s);
+    check_launch("band order");
+    c.sync();
+}
+
+void gs_sweep_cta(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
+                  int dir, bool xold_zero, const int* border, int B) {
+    const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 4.0 * a.n + 24.0 * a.n;
+    Ctx::Scope sc(&c, MPREC_K_GS, bytes);
+    int* ctr = c.counters.p + 7;
+    MG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), c.s));
+    const int nbands = (a.n + B - 1) / B;
+    const size_t smem = size_t(B) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        MG_CUDA(cudaFuncSetAttribute(k_gs_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        MG_CUDA(cudaFuncSetAttribute(k_gs_cta<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    static const int threads = [] {
+        const char* e = getenv("MPREC_GS_CTA_THREADS");
+        return e ? atoi(e) : 1024;
+    }();
+    const int grid = std::max(1, std::min(nbands, c.sm_count * std::max(1, 2048 / threads)));
+    if (dir > 0)
+        k_gs_cta<1><<<grid, threads, smem, c.s>>>(a.rp, a.ci, a.v, invd, b, xold_zero ? nullptr : xold, xnew, border, a.n,
+                                              B, nbands, ctr);
+    else
+        k_gs_cta<-1><<<grid, threads, smem, c.s>>>(a.rp, a.ci, a.v, invd, b, xold_zero ? nullptr : xold, xnew, border,
+                                               a.n, B, nbands, ctr);
+    check_launch("gs_sweep_cta");
+}
+
 void compute_invd(Ctx& c, const CsrView& a, double* invd) {
     k_invd<<<(a.n + 255) / 256, 256, 0, c.s>>>(a.v, a.diag, a.n, invd);
     check_launch("invd");
@@ -164,6 +295,8 @@ static void level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold
     const BandSched& bs = dir > 0 ? L.band_fwd : L.band_bwd;
     if (bs.ok)
         gs_band_sweep(c, bs, L.a.nnz, L.n, r, zero ? nullptr : xold, xnew);
+    else if (L.cta_B > 0)
+        gs_sweep_cta(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.border_f.p : L.border_b.p, L.cta_B);
     else
         gs_sweep(c, L.a, r, xold, xnew, dir, zero, dir > 0 ? L.ofwd : L.obwd, L.invd.p);
 }
@@ -248,5 +381,61 @@ void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
+}
+}  // namespace mg
+
+namespace mg {
+// Setup-time choice of the sweep kernel for one level (measure, don't guess):
+// row-per-warp (cross-SM hops) vs CTA bands of 4096 / 8192 rows (on-SM hops).
+void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
+    L.cta_B = 0;
+    if (L.n < 65536) return;
+    static const int mode = [] {
+        const char* e = getenv("MPREC_GS_CTA_ROWS");
+        return e ? atoi(e) : -1;  // -1: autotune, 0: off, >0: fixed band size
+    }();
+    if (mode == 0) return;
+    fill(c, L.b.p, 1.0, L.n);
+    cudaEvent_t e0, e1;
+    MG_CUDA(cudaEventCreate(&e0));
+    MG_CUDA(cudaEventCreate(&e1));
+    auto time_fwd = [&]() {
+        float best = 1e30f;
+        for (int rep = 0; rep < 2; ++rep) {
+            fill_pending(c, L.xf.p, L.n);
+            cudaEventRecord(e0, c.s);
+            level_sweep(c, L, L.b.p, nullptr, L.xf.p, +1, true);
+            cudaEventRecord(e1, c.s);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = std::min(best, ms);
+        }
+        return best;
+    };
+    float t_best = time_fwd();
+    int b_best = 0;
+    const int cand[2] = {4096, 8192};
+    for (int bsz : (mode > 0 ? std::vector<int>{mode} : std::vector<int>{cand[0], cand[1]})) {
+        if (L.n < 2 * bsz) continue;
+        L.cta_B = bsz;
+        build_band_order(c, L.n, sf.level.p, bsz, L.border_f);
+        const float t = time_fwd();
+        if (mode > 0 || t < t_best) {
+            t_best = t;
+            b_best = bsz;
+        }
+    }
+    L.cta_B = b_best;
+    if (b_best) {
+        build_band_order(c, L.n, sf.level.p, b_best, L.border_f);
+        build_band_order(c, L.n, sb.level.p, b_best, L.border_b);
+    } else {
+        L.border_f.release();
+        L.border_b.release();
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: %s (%.3f ms fwd)\n", L.n, b_best ? "cta-band" : "row-per-warp", t_best);
 }
 }  // namespace mg

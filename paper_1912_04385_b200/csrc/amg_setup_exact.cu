@@ -906,6 +906,9 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
             }
             l.invd.alloc(std::max(l.n, 1));
             compute_invd(c, l.a, l.invd.p);
+            l.b.ensure(std::max(l.n, 1));
+            l.xf.ensure(std::max(l.n, 1));
+            tune_level_sweep(c, l, (li == 0 && pat) ? pat->fwd : l.own_fwd, (li == 0 && pat) ? pat->bwd : l.own_bwd);
         }
     }
     {

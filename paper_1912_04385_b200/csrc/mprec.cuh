@@ -163,6 +163,8 @@ struct AmgLevel {
     const int* obwd = nullptr;
     BandSched band_fwd, band_bwd;     // band schedules (opt-in, MPREC_GS_BAND=1)
     DBuf<double> invd;                // 1 / a_ii
+    int cta_B = 0;                    // CTA-band sweep: rows per band (0: row-per-warp sweep)
+    DBuf<int> border_f, border_b;     // band rows in global level order (fwd / bwd)
 };
 
 struct Amg {
@@ -191,5 +193,7 @@ void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, dou
               bool xold_zero, const int* order, const double* invd = nullptr);
 void dense_gemv(Ctx& c, const double* m_rowmajor, int n, const double* x, double* y);
 void compute_invd(Ctx& c, const CsrView& a, double* invd);
+void build_band_order(Ctx& c, int n, const int* lev, int B, DBuf<int>& border);
+void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb);
 
 }  // namespace mg
