@@ -11,6 +11,7 @@
 // (double buffering also makes the "old" reads race-free for any pattern).
 #include <cub/cub.cuh>
 #include <cstdlib>
+#include <string>
 
 #include "mprec.cuh"
 
@@ -77,12 +78,6 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp
     }
 }
 
-// CTA per band of B consecutive rows (doacross).  The band's new
-// iterate lives in shared memory (kPending sentinel), so dependencies inside
-// the band are resolved by an on-SM poll instead of an L2 round trip; rows of
-// the band are claimed by the CTA's warps in global DAG-level order (`border`)
-// and bands are claimed in sweep order, hence deadlock-free.  Row arithmetic
-// is identical to k_gs (warp per row).
 // CTA per band of B consecutive rows (doacross).  The band's new
 // iterate lives in shared memory (kPending sentinel), so dependencies inside
 // the band are resolved by an on-SM poll instead of an L2 round trip; rows of
@@ -295,6 +290,8 @@ static void level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold
     const BandSched& bs = dir > 0 ? L.band_fwd : L.band_bwd;
     if (bs.ok)
         gs_band_sweep(c, bs, L.a.nnz, L.n, r, zero ? nullptr : xold, xnew);
+    else if (L.seg)
+        gs_sweep_seg(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.seg_fwd : L.seg_bwd);
     else if (L.cta_B > 0)
         gs_sweep_cta(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.border_f.p : L.border_b.p, L.cta_B);
     else
@@ -386,15 +383,30 @@ void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int
 
 namespace mg {
 // Setup-time choice of the sweep kernel for one level (measure, don't guess):
-// row-per-warp (cross-SM hops) vs CTA bands of 4096 / 8192 rows (on-SM hops).
+// row-per-warp (cross-SM hops), CTA bands of 4096 / 8192 rows (on-SM hops) or
+// 32-row segment chains (gs_seg.cu).  MPREC_GS_MODE forces one: warp | cta | seg.
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     L.cta_B = 0;
-    if (L.n < 65536) return;
-    static const int mode = [] {
-        const char* e = getenv("MPREC_GS_CTA_ROWS");
-        return e ? atoi(e) : -1;  // -1: autotune, 0: off, >0: fixed band size
+    L.seg = false;
+    const std::string force = [] {  // read per setup so tests can force each kernel
+        const char* e = getenv("MPREC_GS_MODE");
+        return std::string(e ? e : "");
     }();
-    if (mode == 0) return;
+    if (force == "warp") return;
+    const bool sorted = csr_sorted(c, L.a);
+    if (force == "seg") {
+        if (!sorted) return;
+        const int bsz = [] {
+            const char* e = getenv("MPREC_GS_SEG_B");
+            return e ? atoi(e) : 8192;
+        }();
+        build_seg_sched(c, L.a, L.seg_fwd, L.seg_bwd);
+        build_seg_bands(c, L.seg_fwd, bsz);
+        build_seg_bands(c, L.seg_bwd, bsz);
+        L.seg = true;
+        return;
+    }
+    if (L.n < 4096 && force.empty()) return;
     fill(c, L.b.p, 1.0, L.n);
     cudaEvent_t e0, e1;
     MG_CUDA(cudaEventCreate(&e0));
@@ -413,21 +425,50 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         }
         return best;
     };
-    float t_best = time_fwd();
-    int b_best = 0;
-    const int cand[2] = {4096, 8192};
-    for (int bsz : (mode > 0 ? std::vector<int>{mode} : std::vector<int>{cand[0], cand[1]})) {
-        if (L.n < 2 * bsz) continue;
-        L.cta_B = bsz;
-        build_band_order(c, L.n, sf.level.p, bsz, L.border_f);
-        const float t = time_fwd();
-        if (mode > 0 || t < t_best) {
-            t_best = t;
-            b_best = bsz;
+    const char* names[3] = {"row-per-warp", "cta-band", "band-segment"};
+    int best_mode = 0, b_best = 0;
+    float t_best = force.empty() ? time_fwd() : 1e30f;
+    if (force.empty() || force == "cta") {
+        for (int bsz : {4096, 8192}) {
+            if (L.n < 2 * bsz) continue;
+            L.cta_B = bsz;
+            build_band_order(c, L.n, sf.level.p, bsz, L.border_f);
+            const float t = time_fwd();
+            if (t < t_best) {
+                t_best = t;
+                b_best = bsz;
+                best_mode = 1;
+            }
         }
+        L.cta_B = 0;
     }
-    L.cta_B = b_best;
-    if (b_best) {
+    int seg_best = 0;
+    if (sorted && (force.empty() || force == "seg")) {
+        build_seg_sched(c, L.a, L.seg_fwd, L.seg_bwd);
+        L.seg = true;
+        for (int bsz : {4096, 8192, 16384}) {
+            build_seg_bands(c, L.seg_fwd, bsz);
+            const float t = time_fwd();
+            if (t < t_best) {
+                t_best = t;
+                best_mode = 2;
+                seg_best = bsz;
+            }
+            if (L.n <= bsz) break;
+        }
+        L.seg = false;
+    }
+    if (best_mode != 2) {
+        L.seg_fwd = SegSched();
+        L.seg_bwd = SegSched();
+    }
+    L.seg = best_mode == 2;
+    if (L.seg) {
+        build_seg_bands(c, L.seg_fwd, seg_best);
+        build_seg_bands(c, L.seg_bwd, seg_best);
+    }
+    L.cta_B = best_mode == 1 ? b_best : 0;
+    if (best_mode == 1) {
         build_band_order(c, L.n, sf.level.p, b_best, L.border_f);
         build_band_order(c, L.n, sb.level.p, b_best, L.border_b);
     } else {
@@ -436,6 +477,8 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: %s (%.3f ms fwd)\n", L.n, b_best ? "cta-band" : "row-per-warp", t_best);
+    if (trace_on())
+        fprintf(stderr, "[mprec] level n=%d sweep: %s B=%d (%.3f ms fwd)\n", L.n, names[best_mode],
+                best_mode == 2 ? seg_best : L.cta_B, t_best);
 }
 }  // namespace mg

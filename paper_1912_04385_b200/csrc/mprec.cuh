@@ -38,6 +38,15 @@ struct Sched {
     int n = 0;
     int nlev = 0;
 };
+// Segment-chain sweep schedule (gs_seg.cu): segments [start[s], start[s+1])
+// are dependency chains of <= 32 rows; sched orders the segments.
+struct SegSched {
+    DBuf<int> start;
+    Sched sched;
+    std::vector<int> hstart;        // host copy of start
+    int B = 0, nbands = 0, band_rows = 0;
+    DBuf<int> bord, bseg0, brow0;   // band-local segment order, band -> first segment / first row
+};
 // dir = +1: row i depends on stored k < i; dir = -1: on stored k > i.
 void build_sched(Ctx& c, int n, const int* rp, const int* ci, int dir, Sched& out);
 
@@ -165,6 +174,8 @@ struct AmgLevel {
     DBuf<double> invd;                // 1 / a_ii
     int cta_B = 0;                    // CTA-band sweep: rows per band (0: row-per-warp sweep)
     DBuf<int> border_f, border_b;     // band rows in global level order (fwd / bwd)
+    bool seg = false;                 // segment-chain sweep (gs_seg.cu)
+    SegSched seg_fwd, seg_bwd;        // segment bounds + claim orders (fwd / bwd)
 };
 
 struct Amg {
@@ -194,6 +205,11 @@ void gs_sweep(Ctx& c, const CsrView& a, const double* b, const double* xold, dou
 void dense_gemv(Ctx& c, const double* m_rowmajor, int n, const double* x, double* y);
 void compute_invd(Ctx& c, const CsrView& a, double* invd);
 void build_band_order(Ctx& c, int n, const int* lev, int B, DBuf<int>& border);
+bool csr_sorted(Ctx& c, const CsrView& a);
+void build_seg_sched(Ctx& c, const CsrView& a, SegSched& fwd, SegSched& bwd);
+void build_seg_bands(Ctx& c, SegSched& seg, int B);
+void gs_sweep_seg(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
+                  int dir, bool xold_zero, const SegSched& seg);
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb);
 
 }  // namespace mg
