@@ -384,7 +384,7 @@ void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int
 namespace mg {
 // Setup-time choice of the sweep kernel for one level (measure, don't guess):
 // row-per-warp (cross-SM hops), CTA bands of 4096 / 8192 rows (on-SM hops) or
-// 32-row segment chains (gs_seg.cu).  MPREC_GS_MODE forces one: warp | cta | seg.
+// band-segment chains (gs_seg.cu).  MPREC_GS_MODE forces one: warp | cta | seg.
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     L.cta_B = 0;
     L.seg = false;
@@ -393,6 +393,11 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         return std::string(e ? e : "");
     }();
     if (force == "warp") return;
+    // candidates by size (B200 measurements): the band kernels only
+    // win on the finest, million-row levels; below that no timing is needed
+    const bool try_cta = !force.empty() || L.n >= (1 << 20);
+    const bool try_seg = !force.empty() || L.n >= (2 << 20);
+    if (force.empty() && !try_cta && !try_seg) return;
     const bool sorted = csr_sorted(c, L.a);
     if (force == "seg") {
         if (!sorted) return;
@@ -406,7 +411,6 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         L.seg = true;
         return;
     }
-    if (L.n < 4096 && force.empty()) return;
     fill(c, L.b.p, 1.0, L.n);
     cudaEvent_t e0, e1;
     MG_CUDA(cudaEventCreate(&e0));
@@ -428,7 +432,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     const char* names[3] = {"row-per-warp", "cta-band", "band-segment"};
     int best_mode = 0, b_best = 0;
     float t_best = force.empty() ? time_fwd() : 1e30f;
-    if (force.empty() || force == "cta") {
+    if ((force.empty() && try_cta) || force == "cta") {
         for (int bsz : {4096, 8192}) {
             if (L.n < 2 * bsz) continue;
             L.cta_B = bsz;
@@ -443,10 +447,10 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         L.cta_B = 0;
     }
     int seg_best = 0;
-    if (sorted && (force.empty() || force == "seg")) {
+    if (sorted && ((force.empty() && try_seg) || force == "seg")) {
         build_seg_sched(c, L.a, L.seg_fwd, L.seg_bwd);
         L.seg = true;
-        for (int bsz : {4096, 8192, 16384}) {
+        for (int bsz : {4096, 8192}) {
             build_seg_bands(c, L.seg_fwd, bsz);
             const float t = time_fwd();
             if (t < t_best) {

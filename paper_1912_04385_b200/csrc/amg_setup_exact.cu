@@ -163,12 +163,41 @@ __global__ void k_max_int(const int* a, int n, int* out) {
     if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
+constexpr int kRsList = 512;  // per-selection lists kept in smem (overflow spills to global)
+
 // One warp: exact emulation of the lazy-heap greedy (amg.cpp:86-111).
+// SMEM: the bucket counts and the two summary levels of the bitmaps live in
+// shared memory (copied in at start), so of the per-selection dependent memory
+// round trips only the bottom bitmap level and the per-point arrays (mark,
+// lambda, increments; L2-resident) go off-chip.  The selection order -- highest
+// bucket, lowest index -- and hence the C/F splitting are unchanged.
+template <bool SMEM>
 __global__ void __launch_bounds__(32) k_rs_select(const int* srp, const int* sci, const int* strp, const int* stci,
                                                   signed char* mark, int* lam, Buckets q, int nbuckets, int* inc,
-                                                  int* jlist, int* klist) {
+                                                  int* jlist, int* klist, long long* prof) {
+    extern __shared__ unsigned long long bq_sm[];
+    long long pf[6] = {0, 0, 0, 0, 0, 0}, tp = clock64(), iters = 0;
+#define RS_LAP(k)                          \
+    if (prof) {                            \
+        const long long tn = clock64();    \
+        pf[k] += tn - tp;                  \
+        tp = tn;                           \
+    }
     const int lane = threadIdx.x;
     __shared__ int nj_sh, nk_sh;
+    __shared__ int js0[kRsList], js1[kRsList], kid[kRsList], klam[kRsList];
+    if (SMEM) {
+        unsigned long long* s1 = bq_sm;
+        unsigned long long* s2 = s1 + (size_t)nbuckets * q.n1;
+        int* sc = reinterpret_cast<int*>(s2 + (size_t)nbuckets * q.n2);
+        for (int t = lane; t < nbuckets * q.n1; t += 32) s1[t] = q.l1[t];
+        for (int t = lane; t < nbuckets * q.n2; t += 32) s2[t] = q.l2[t];
+        for (int t = lane; t < nbuckets; t += 32) sc[t] = q.cnt[t];
+        q.l1 = s1;
+        q.l2 = s2;
+        q.cnt = sc;
+        __syncwarp();
+    }
     int hi = nbuckets - 1;
     for (;;) {
         // highest non-empty bucket
@@ -183,7 +212,14 @@ __global__ void __launch_bounds__(32) k_rs_select(const int* srp, const int* sci
             hi -= 32;
             if (hi < 0) break;
         }
-        if (hi < 0) return;
+        if (hi < 0) {
+            if (prof && lane == 0) {
+                for (int k = 0; k < 6; ++k) prof[k] = pf[k];
+                prof[6] = iters;
+            }
+            return;
+        }
+        ++iters;
         // lowest index in bucket hi: first non-zero top-level word
         int first = 0x7fffffff;
         for (int w = lane; w < q.n2; w += 32)
@@ -207,40 +243,86 @@ __global__ void __launch_bounds__(32) k_rs_select(const int* srp, const int* sci
         }
         i = __shfl_sync(0xffffffffu, i, 0);
         __syncwarp();
-        // phase d: undecided j in S^T_i become F
-        for (int jj = strp[i] + lane; jj < strp[i + 1]; jj += 32) {
-            const int j = stci[jj];
-            if (((volatile signed char*)mark)[j] == kU) {
-                mark[j] = kF;
-                bq_remove(q, j, lam[j]);
-                jlist[atomicAdd(&nj_sh, 1)] = j;
-            }
-        }
-        __syncwarp();
-        const int nj = ((volatile int*)&nj_sh)[0];
-        // phase e1: count the increments of every undecided k in S_j
-        for (int t = 0; t < nj; ++t) {
-            const int j = jlist[t];
-            for (int kk = srp[j] + lane; kk < srp[j + 1]; kk += 32) {
-                const int k = sci[kk];
-                if (((volatile signed char*)mark)[k] == kU) {
-                    if (atomicAdd(inc + k, 1) == 0) klist[atomicAdd(&nk_sh, 1)] = k;
+        RS_LAP(0)
+        // phase d: undecided j in S^T_i become F.  The loads a later phase needs
+        // (lambda_j, the bounds of S_j) are issued together with mark[j].
+        {
+            const int a0 = strp[i], a1 = strp[i + 1];
+            for (int jj = a0 + lane; jj < a1; jj += 32) {
+                const int j = stci[jj];
+                const signed char mj = ((volatile signed char*)mark)[j];
+                const int lj = lam[j], s0 = srp[j], s1 = srp[j + 1];
+                if (mj == kU) {
+                    mark[j] = kF;
+                    bq_remove(q, j, lj);
+                    const int t = atomicAdd(&nj_sh, 1);
+                    if (t < kRsList) {
+                        js0[t] = s0;
+                        js1[t] = s1;
+                    } else {
+                        jlist[2 * (t - kRsList)] = s0;
+                        jlist[2 * (t - kRsList) + 1] = s1;
+                    }
                 }
             }
         }
         __syncwarp();
-        const int nk = ((volatile int*)&nk_sh)[0];
-        // phase e2a: removals
-        for (int t = lane; t < nk; t += 32) {
-            const int k = klist[t];
-            bq_remove(q, k, lam[k]);
+        RS_LAP(1)
+        const int nj = ((volatile int*)&nj_sh)[0];
+        // phase e1: count the increments of every undecided k in S_j; 4 rows at a
+        // time, 8 lanes per row (the rows' memory round trips overlap)
+        {
+            const int grp = lane >> 3, sub = lane & 7;
+            for (int t0 = 0; t0 < nj; t0 += 4) {
+                const int t = t0 + grp;
+                if (t < nj) {
+                    const int s0 = t < kRsList ? js0[t] : jlist[2 * (t - kRsList)];
+                    const int s1 = t < kRsList ? js1[t] : jlist[2 * (t - kRsList) + 1];
+                    for (int kk = s0 + sub; kk < s1; kk += 8) {
+                        const int k = sci[kk];
+                        const signed char mk = ((volatile signed char*)mark)[k];
+                        const int lk = lam[k];
+                        if (mk == kU && atomicAdd(inc + k, 1) == 0) {
+                            const int u = atomicAdd(&nk_sh, 1);
+                            if (u < kRsList) {
+                                kid[u] = k;
+                                klam[u] = lk;
+                            } else {
+                                klist[2 * (u - kRsList)] = k;
+                                klist[2 * (u - kRsList) + 1] = lk;
+                            }
+                        }
+                    }
+                }
+            }
         }
         __syncwarp();
-        // phase e2b: insertions at the incremented lambda
+        RS_LAP(2)
+        const int nk = ((volatile int*)&nk_sh)[0];
+        // phase e2: removals (all), then insertions at the incremented lambda; a
+        // removal and an insertion may share a bitmap word, hence two phases
         int mx = -1;
+        int k0 = 0, lk0 = 0, ik0 = 0;  // first 32 candidates stay in registers
         for (int t = lane; t < nk; t += 32) {
-            const int k = klist[t];
-            const int nl = lam[k] + ((volatile int*)inc)[k];
+            const int k = t < kRsList ? kid[t] : klist[2 * (t - kRsList)];
+            const int lk = t < kRsList ? klam[t] : klist[2 * (t - kRsList) + 1];
+            if (t < 32) {
+                k0 = k;
+                lk0 = lk;
+                ik0 = ((volatile int*)inc)[k];  // overlaps the removal below
+            }
+            bq_remove(q, k, lk);
+        }
+        __syncwarp();
+        RS_LAP(3)
+        for (int t = lane; t < nk; t += 32) {
+            int k = k0, lk = lk0, ik = ik0;
+            if (t >= 32) {
+                k = t < kRsList ? kid[t] : klist[2 * (t - kRsList)];
+                lk = t < kRsList ? klam[t] : klist[2 * (t - kRsList) + 1];
+                ik = ((volatile int*)inc)[k];
+            }
+            const int nl = lk + ik;
             inc[k] = 0;
             lam[k] = nl;
             bq_insert(q, k, nl);
@@ -249,7 +331,9 @@ __global__ void __launch_bounds__(32) k_rs_select(const int* srp, const int* sci
         for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         hi = max(hi, mx);
         __syncwarp();
+        RS_LAP(4)
     }
+#undef RS_LAP
 }
 
 // --------------------------------------------- RS second and third passes --
@@ -766,7 +850,7 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
     q.n1 = (q.n0 + 63) / 64;
     q.n2 = (q.n1 + 63) / 64;
     DBuf<unsigned long long> l0((size_t)nbuckets * q.n0), l1((size_t)nbuckets * q.n1), l2((size_t)nbuckets * q.n2);
-    DBuf<int> bcnt(nbuckets), lam(n), inc(n), jlist(n), klist(n);
+    DBuf<int> bcnt(nbuckets), lam(n), inc(n), jlist(2 * (size_t)n), klist(2 * (size_t)n);
     MG_CUDA(cudaMemsetAsync(l0.p, 0, l0.bytes(), c.s));
     MG_CUDA(cudaMemsetAsync(bcnt.p, 0, bcnt.bytes(), c.s));
     MG_CUDA(cudaMemsetAsync(inc.p, 0, inc.bytes(), c.s));
@@ -782,9 +866,30 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
     {
         Trace tr(&c, "amg rs first pass");
         Ctx::Scope sc(&c, MPREC_K_BLAS1, 0.0);
-        k_rs_select<<<1, 32, 0, c.s>>>(srp.p, sci.p, strp.p, stci.p, mark, lam.p, q, nbuckets, inc.p, jlist.p,
-                                       klist.p);
+        const size_t smem = sizeof(unsigned long long) * (size_t)nbuckets * (q.n1 + q.n2) + sizeof(int) * nbuckets;
+        DBuf<long long> prof;
+        if (trace_on()) prof.alloc(8);
+        if (smem <= 200 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                MG_CUDA(cudaFuncSetAttribute(k_rs_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                attr = true;
+            }
+            k_rs_select<true><<<1, 32, smem, c.s>>>(srp.p, sci.p, strp.p, stci.p, mark, lam.p, q, nbuckets, inc.p,
+                                                    jlist.p, klist.p, prof.p);
+        } else {
+            k_rs_select<false><<<1, 32, 0, c.s>>>(srp.p, sci.p, strp.p, stci.p, mark, lam.p, q, nbuckets, inc.p,
+                                                  jlist.p, klist.p, prof.p);
+        }
         check_launch("rs first pass");
+        if (trace_on()) {
+            long long h[7];
+            prof.download(h, 7, c.s);
+            c.sync();
+            fprintf(stderr, "[mprec] rs select n=%d sel=%lld cycles/sel: find %.0f  d %.0f  e1 %.0f  e2a %.0f  e2b %.0f\n", n,
+                    h[6], h[0] / double(h[6]), h[1] / double(h[6]), h[2] / double(h[6]), h[3] / double(h[6]),
+                    h[4] / double(h[6]));
+        }
     }
     // ---- second pass
     Trace tr2(&c, "amg rs passes 2+3");
