@@ -93,9 +93,32 @@ typedef struct mprec_solve_result {
     int total_iterations;       /* summed over all attempts */
 } mprec_solve_result;
 
+/* GlobalJacobian (condense.hpp:64-81) in plain arrays.  Primary blocks are
+ * uniform np x np in the canonical (s..., P, T) order (FieldLayout::uniform);
+ * cell c has sec_off[c+1]-sec_off[c] secondary unknowns.  All dense blocks
+ * are column-major and packed in cell / entry order:
+ *   j22: sum ns_c^2, j21: ns_c x np per cell, j12 entry e: np x ns_{col[e]},
+ *   r1: n_cells*np, r2: sec_off[n_cells]. */
+typedef struct mprec_global_jacobian {
+    int n_cells, np;
+    const int* row_ptr;  /* J11 block CSR (n_cells+1), sorted columns, diagonal present */
+    const int* col_idx;
+    const double* j11;
+    const int* sec_off;  /* n_cells+1 */
+    const double* j22;
+    const double* j21;
+    int n_j12;
+    const int* j12_row;
+    const int* j12_col;
+    const double* j12;
+    const double* r1;
+    const double* r2;
+} mprec_global_jacobian;
+
 typedef struct mprec_gpu_system mprec_gpu_system; /* opaque */
 typedef struct mprec_gpu_amg mprec_gpu_amg;       /* opaque */
 typedef struct mprec_gpu_ilu mprec_gpu_ilu;       /* opaque */
+typedef struct mprec_gpu_condensed mprec_gpu_condensed; /* opaque */
 
 const char* mprec_gpu_last_error(void);
 int mprec_gpu_error_payload(void);
@@ -153,6 +176,23 @@ int mprec_gpu_get_matrix(mprec_gpu_system* h, int* row_ptr, int* col_idx, double
 /* write_block_matrix + write_vector (matrix_io.cpp:93-114), %.17g round-trip exact */
 int mprec_gpu_write_system(mprec_gpu_system* h, const char* matrix_path, const char* layout_path,
                            const char* rhs_path);
+
+/* ---- static condensation (condense.hpp:92-107, condense.cpp:206-258) ----
+ * condense: per-cell partial-pivot LU of J22 (SingularBlockError(cell,
+ * "secondary") when |u_ii| <= 1e-14 * max|J22_c|, first failing cell),
+ * A = J11 - J12 J22^-1 J21 assembled like BlockMatrix::assemble (duplicate
+ * blocks summed in entry order: J11 first, then the J12 list),
+ * b = -r1 + J12 J22^-1 r2.  Everything stays on the device; the J22 factors
+ * are kept for back_substitute. */
+int mprec_gpu_condense(const mprec_global_jacobian* j, mprec_gpu_condensed** out);
+int mprec_gpu_condensed_shape(mprec_gpu_condensed* h, int* n_cells, int* np, int* nnzb, int* n_secondary);
+/* reduced system A (BSR, column-major blocks) and b (any may be NULL) */
+int mprec_gpu_condensed_get(mprec_gpu_condensed* h, int* row_ptr, int* col_idx, double* values, double* b);
+/* a solver handle on the reduced system (device to device); its rhs is b */
+int mprec_gpu_condensed_system(mprec_gpu_condensed* h, mprec_gpu_system** out);
+/* d2 = J22^-1 (-r2 - J21 d1) per cell (condense.cpp:243-258); host buffers */
+int mprec_gpu_back_substitute(mprec_gpu_condensed* h, const double* d1, double* d2);
+void mprec_gpu_condensed_destroy(mprec_gpu_condensed* h);
 
 /* Parity diagnostics. */
 int mprec_gpu_get_scaled(mprec_gpu_system* h, double* abar_values, double* b_bar);

@@ -3,6 +3,8 @@
 // multiply followed by a rounded add, as the reference's scalar loops are.
 #include "oracle.hpp"
 
+#include <map>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -1067,6 +1069,102 @@ std::vector<int> level_sets_lower(const Csr& a) {
         lev[i] = l;
     }
     return lev;
+}
+
+// ======================================================= condensation ==
+// condense.cpp:206-241.  Per cell: PartialPivLU of J22 (DenseLU, Eigen's
+// unblocked order) with the 1e-14 relative pivot test; entries = J11 blocks,
+// then -J12_e (J22_c^-1 J21_c) in J12 list order, merged like
+// BlockMatrix::assemble (std::map on (row, col), duplicates summed in entry
+// order); b = -r1 + J12_e (J22_c^-1 r2_c).  Small products sum k ascending
+// from the first term.
+ReducedSystem condense(const GlobalJacobian& j) {
+    const int nc = j.nc, np = j.np;
+    ReducedSystem red;
+    red.nc = nc;
+    red.np = np;
+    red.sec_off = j.sec_off;
+    red.j21 = j.j21;
+    red.r2 = j.r2;
+    red.lu.resize(nc);
+    for (int c = 0; c < nc; ++c) {
+        const int ns = j.sec_off[c + 1] - j.sec_off[c];
+        if (ns == 0) continue;
+        red.lu[c].factor(j.j22[c].data(), ns);
+        double scale = 0.0;
+        for (double v : j.j22[c]) scale = std::max(scale, std::abs(v));
+        if (!red.lu[c].pivots_ok(1e-14 * (scale > 0.0 ? scale : 1.0), nullptr))
+            throw Error(SINGULAR_BLOCK, "singular secondary block", c);
+    }
+    const size_t bs = size_t(np) * np;
+    std::map<std::pair<int, int>, Vec> merged;
+    auto add = [&](int r, int c, const double* blk) {
+        auto key = std::make_pair(r, c);
+        auto it = merged.find(key);
+        if (it == merged.end()) {
+            merged.emplace(key, Vec(blk, blk + bs));
+        } else {
+            for (size_t e = 0; e < bs; ++e) it->second[e] = it->second[e] + blk[e];
+        }
+    };
+    for (int r = 0; r < nc; ++r)
+        for (int k = j.rp[r]; k < j.rp[r + 1]; ++k) add(r, j.ci[k], &j.j11[size_t(k) * bs]);
+    red.b.resize(size_t(nc) * np);
+    for (size_t e = 0; e < red.b.size(); ++e) red.b[e] = -j.r1[e];
+    for (size_t e = 0; e < j.e_row.size(); ++e) {
+        const int r = j.e_row[e], c = j.e_col[e];
+        const int ns = j.sec_off[c + 1] - j.sec_off[c];
+        if (ns == 0) continue;
+        // X = J22^-1 [J21 | r2]  (ns x (np+1))
+        Vec x(size_t(ns) * (np + 1));
+        for (int q = 0; q <= np; ++q) {
+            double* col = &x[size_t(q) * ns];
+            for (int i = 0; i < ns; ++i) col[i] = q < np ? j.j21[c][size_t(q) * ns + i] : j.r2[c][i];
+            red.lu[c].solve_inplace(col);
+        }
+        const Vec& a = j.e_blk[e];  // np x ns
+        Vec corr(bs);
+        for (int q = 0; q <= np; ++q)
+            for (int i = 0; i < np; ++i) {
+                double acc = a[i] * x[size_t(q) * ns];
+                for (int k = 1; k < ns; ++k) acc = acc + a[size_t(k) * np + i] * x[size_t(q) * ns + k];
+                if (q < np)
+                    corr[size_t(q) * np + i] = -acc;
+                else
+                    red.b[size_t(r) * np + i] = red.b[size_t(r) * np + i] + acc;
+            }
+        add(r, c, corr.data());
+    }
+    // BlockMatrix::assemble: diagonal blocks always present
+    for (int c = 0; c < nc; ++c)
+        if (merged.find({c, c}) == merged.end()) merged.emplace(std::make_pair(c, c), Vec(bs, 0.0));
+    red.rp.assign(nc + 1, 0);
+    for (const auto& [key, blk] : merged) {
+        red.ci.push_back(key.second);
+        red.a.insert(red.a.end(), blk.begin(), blk.end());
+        red.rp[key.first + 1]++;
+    }
+    for (int r = 0; r < nc; ++r) red.rp[r + 1] += red.rp[r];
+    return red;
+}
+
+// condense.cpp:243-258: d2_c = J22_c^-1 (-r2_c - J21_c d1_c)
+Vec back_substitute(const ReducedSystem& r, const Vec& d1) {
+    if (int64_t(d1.size()) != int64_t(r.nc) * r.np) throw Error(DIMENSION, "primary update dimension mismatch");
+    Vec d2(size_t(r.sec_off[r.nc]));
+    for (int c = 0; c < r.nc; ++c) {
+        const int s0 = r.sec_off[c], ns = r.sec_off[c + 1] - s0;
+        if (ns == 0) continue;
+        Vec t(ns);
+        for (int i = 0; i < ns; ++i) {
+            double acc = r.j21[c][i] * d1[size_t(c) * r.np];
+            for (int k = 1; k < r.np; ++k) acc = acc + r.j21[c][size_t(k) * ns + i] * d1[size_t(c) * r.np + k];
+            t[i] = -r.r2[c][i] - acc;
+        }
+        r.lu[c].solve_inplace(t.data());
+        for (int i = 0; i < ns; ++i) d2[s0 + i] = t[i];
+    }
+    return d2;
 }
 
 }  // namespace oracle

@@ -231,4 +231,32 @@ SolveOutcome solve_system(const Bsr& a, const Vec& b, Method m, double tol = 1e-
 // GPU sweeps must honour.
 std::vector<int> level_sets_lower(const Csr& a);
 
+// ----- static condensation (proj/src/condense.cpp:206-258) ------------------
+// GlobalJacobian (condense.hpp:64-81) with uniform np x np primary blocks;
+// dense blocks column-major.
+struct GlobalJacobian {
+    int nc = 0, np = 0;
+    std::vector<int> rp, ci;             // J11 block pattern
+    Vec j11;                             // nnzb * np * np
+    std::vector<int> sec_off;            // nc + 1
+    std::vector<Vec> j22, j21;           // per cell: ns x ns, ns x np
+    std::vector<int> e_row, e_col;       // J12 entries (list order)
+    std::vector<Vec> e_blk;              // np x ns_col
+    Vec r1;                              // nc * np
+    std::vector<Vec> r2;                 // per cell
+};
+struct ReducedSystem {
+    int nc = 0, np = 0;
+    std::vector<int> rp, ci;
+    Vec a;                               // nnzb * np * np
+    Vec b;
+    std::vector<DenseLU> lu;
+    std::vector<Vec> j21, r2;
+    std::vector<int> sec_off;
+};
+// condense.cpp:206-241 (SINGULAR_BLOCK "secondary" with the cell id)
+ReducedSystem condense(const GlobalJacobian& j);
+// condense.cpp:243-258
+Vec back_substitute(const ReducedSystem& r, const Vec& d1);
+
 }  // namespace oracle

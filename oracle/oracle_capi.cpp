@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <string>
 
 #include "../include/mprec_gpu.h"
@@ -72,6 +73,9 @@ struct orc_system {
 };
 struct orc_amg {
     AMGHierarchy h;
+};
+struct orc_condensed {
+    ReducedSystem r;
 };
 struct orc_ilu {
     Ilu0Block f;
@@ -306,6 +310,80 @@ int orc_ingest(const char* mtx, const char* layout, const char* rhs, orc_system*
         *out = h;
     });
 }
+
+int orc_condense(const mprec_global_jacobian* j, orc_condensed** out) {
+    return guard([&] {
+        if (!j || !out) throw Error(DIMENSION, "null argument");
+        GlobalJacobian g;
+        g.nc = j->n_cells;
+        g.np = j->np;
+        const int nc = g.nc, np = g.np;
+        const int nnzb = j->row_ptr[nc];
+        g.rp.assign(j->row_ptr, j->row_ptr + nc + 1);
+        g.ci.assign(j->col_idx, j->col_idx + nnzb);
+        g.j11.assign(j->j11, j->j11 + size_t(nnzb) * np * np);
+        g.sec_off.assign(j->sec_off, j->sec_off + nc + 1);
+        size_t o22 = 0;
+        for (int c = 0; c < nc; ++c) {
+            const int s0 = g.sec_off[c], ns = g.sec_off[c + 1] - s0;
+            g.j22.emplace_back(j->j22 + o22, j->j22 + o22 + size_t(ns) * ns);
+            o22 += size_t(ns) * ns;
+            g.j21.emplace_back(j->j21 + size_t(s0) * np, j->j21 + size_t(s0 + ns) * np);
+            g.r2.emplace_back(j->r2 + s0, j->r2 + s0 + ns);
+        }
+        size_t o12 = 0;
+        for (int e = 0; e < j->n_j12; ++e) {
+            const int c = j->j12_col[e];
+            const size_t len = size_t(np) * (g.sec_off[c + 1] - g.sec_off[c]);
+            g.e_row.push_back(j->j12_row[e]);
+            g.e_col.push_back(c);
+            g.e_blk.emplace_back(j->j12 + o12, j->j12 + o12 + len);
+            o12 += len;
+        }
+        g.r1.assign(j->r1, j->r1 + size_t(nc) * np);
+        auto h = std::make_unique<orc_condensed>();
+        h->r = condense(g);
+        *out = h.release();
+    });
+}
+
+int orc_condensed_shape(orc_condensed* h, int* n_cells, int* np, int* nnzb, int* n_secondary) {
+    return guard([&] {
+        if (n_cells) *n_cells = h->r.nc;
+        if (np) *np = h->r.np;
+        if (nnzb) *nnzb = h->r.rp[h->r.nc];
+        if (n_secondary) *n_secondary = h->r.sec_off[h->r.nc];
+    });
+}
+
+int orc_condensed_get(orc_condensed* h, int* rp, int* ci, double* vals, double* b) {
+    return guard([&] {
+        if (rp) std::memcpy(rp, h->r.rp.data(), sizeof(int) * h->r.rp.size());
+        if (ci) std::memcpy(ci, h->r.ci.data(), sizeof(int) * h->r.ci.size());
+        if (vals) std::memcpy(vals, h->r.a.data(), sizeof(double) * h->r.a.size());
+        if (b) std::memcpy(b, h->r.b.data(), sizeof(double) * h->r.b.size());
+    });
+}
+
+int orc_condensed_system(orc_condensed* h, orc_system** out) {
+    return guard([&] {
+        const mprec_bsr a{h->r.nc, h->r.np, h->r.rp.data(), h->r.ci.data(), h->r.a.data()};
+        auto s = std::make_unique<orc_system>();
+        s->a = to_bsr(&a);
+        s->b_ingested = h->r.b;
+        *out = s.release();
+    });
+}
+
+int orc_back_substitute(orc_condensed* h, const double* d1, double* d2) {
+    return guard([&] {
+        const Vec x(d1, d1 + size_t(h->r.nc) * h->r.np);
+        const Vec y = back_substitute(h->r, x);
+        if (!y.empty()) std::memcpy(d2, y.data(), sizeof(double) * y.size());
+    });
+}
+
+void orc_condensed_destroy(orc_condensed* h) { delete h; }
 
 int orc_get_shape(orc_system* h, int* n_cells, int* nb, int* nnzb) {
     return guard([&] {

@@ -275,6 +275,12 @@ class Api:
             "get_shape": (C.c_int, [vp, ip, ip, ip]),
             "get_matrix": (C.c_int, [vp, vp, vp, vp, vp]),
             "write_system": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p]),
+            "condense": (C.c_int, [vp, C.POINTER(vp)]),
+            "condensed_shape": (C.c_int, [vp, ip, ip, ip, ip]),
+            "condensed_get": (C.c_int, [vp, vp, vp, vp, vp]),
+            "condensed_system": (C.c_int, [vp, C.POINTER(vp)]),
+            "back_substitute": (C.c_int, [vp, vp, vp]),
+            "condensed_destroy": (None, [vp]),
         }
         self.fn = {}
         for name, (res, args) in list(sig.items()) + list(optional.items()):
@@ -325,6 +331,13 @@ class Api:
         sysm = System.__new__(System)
         sysm.api, sysm.a, sysm.h, sysm.method, sysm.b = self, BlockMatrix(nc.value, nb.value, rp, ci, v), h, None, b
         return sysm
+
+    def condense(self, j) -> "ReducedSystem":
+        """condense (condense.cpp:206-241) of a condense.GlobalJacobian."""
+        gj = j.c_struct()
+        h = C.c_void_p()
+        self.call("condense", C.byref(gj), C.byref(h))
+        return ReducedSystem(self, h)
 
     def gmres(self, a, b, prec=None, tol=1e-8, max_iter=500) -> SolveResult:
         """gmres (gmres.cpp:8-106); a: BlockMatrix or ScalarMatrix; prec: None
@@ -546,3 +559,45 @@ def gpu() -> Api:
             raise ImportError(f"{GPU_LIB} missing: run __graft_entry__.build() (no CPU fallback exists)")
         _gpu_api = Api(GPU_LIB, "mprec_gpu_")
     return _gpu_api
+
+
+class ReducedSystem:
+    """ReducedSystem (condense.hpp:83-90): A = J11 - J12 J22^-1 J21,
+    b = -r1 + J12 J22^-1 r2, with the J22 factors kept for back_substitute."""
+
+    def __init__(self, api: Api, h):
+        self.api, self.h = api, h
+        nc, np_, nnzb, n2 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        api.call("condensed_shape", h, C.byref(nc), C.byref(np_), C.byref(nnzb), C.byref(n2))
+        self.n_cells, self.np, self.n_secondary = nc.value, np_.value, n2.value
+        rp = np.zeros(nc.value + 1, np.int32)
+        ci = np.zeros(nnzb.value, np.int32)
+        v = np.zeros(nnzb.value * np_.value * np_.value)
+        self.b = np.zeros(nc.value * np_.value)
+        api.call("condensed_get", h, _ptr(rp), _ptr(ci), _ptr(v), _ptr(self.b))
+        self.a = BlockMatrix(nc.value, np_.value, rp, ci, v)
+
+    def back_substitute(self, d1) -> np.ndarray:
+        """back_substitute (condense.cpp:243-258): d2 = J22^-1 (-r2 - J21 d1)."""
+        d1 = _f64(d1)
+        if d1.size != self.n_cells * self.np:
+            raise DimensionError("primary update dimension mismatch")
+        d2 = np.zeros(max(self.n_secondary, 1))
+        self.api.call("back_substitute", self.h, _ptr(d1), _ptr(d2))
+        return d2[: self.n_secondary]
+
+    def system(self) -> "System":
+        """A solver System on the reduced A (device to device); its rhs is b."""
+        h = C.c_void_p()
+        self.api.call("condensed_system", self.h, C.byref(h))
+        sysm = System.__new__(System)
+        sysm.api, sysm.a, sysm.h, sysm.method, sysm.b = self.api, self.a, h, None, self.b.copy()
+        return sysm
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.api.fn["condensed_destroy"](self.h)
+                self.h = None
+        except Exception:
+            pass

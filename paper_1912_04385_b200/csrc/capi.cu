@@ -14,6 +14,7 @@
 
 #include <cuda_profiler_api.h>
 
+#include "condense.cuh"
 #include "mprec.cuh"
 
 using namespace mg;
@@ -285,6 +286,12 @@ struct mprec_gpu_ilu {
     Pattern pat;
     Ilu ilu;
     DBuf<double> vals, r, y;
+};
+
+// ====================================================== condensed handle ==
+struct mprec_gpu_condensed {
+    Ctx ctx;
+    Condensed cd;
 };
 
 // ========================================================= system handle ==
@@ -568,6 +575,78 @@ int mprec_gpu_ingest(const char* mtx, const char* layout, const char* rhs, mprec
         *out = h.release();
     });
 }
+
+int mprec_gpu_condense(const mprec_global_jacobian* j, mprec_gpu_condensed** out) {
+    return guard([&] {
+        if (!j || !out) throw Error(MPREC_DIMENSION, "null argument");
+        auto h = std::make_unique<mprec_gpu_condensed>();
+        condense(h->ctx, *j, h->cd);
+        *out = h.release();
+    });
+}
+
+int mprec_gpu_condensed_shape(mprec_gpu_condensed* h, int* n_cells, int* np, int* nnzb, int* n_secondary) {
+    return guard([&] {
+        if (!h) throw Error(MPREC_DIMENSION, "null handle");
+        if (n_cells) *n_cells = h->cd.nc;
+        if (np) *np = h->cd.np;
+        if (nnzb) *nnzb = h->cd.pat.nnzb;
+        if (n_secondary) *n_secondary = h->cd.n2;
+    });
+}
+
+int mprec_gpu_condensed_get(mprec_gpu_condensed* h, int* rp, int* ci, double* vals, double* b) {
+    return guard([&] {
+        if (!h) throw Error(MPREC_DIMENSION, "null handle");
+        const Condensed& d = h->cd;
+        if (rp) std::memcpy(rp, d.pat.h_rp.data(), sizeof(int) * d.pat.h_rp.size());
+        if (ci) std::memcpy(ci, d.pat.h_ci.data(), sizeof(int) * d.pat.h_ci.size());
+        if (vals) d.a_val.download(vals, size_t(d.pat.nnzb) * d.np * d.np, h->ctx.s);
+        if (b) d.b.download(b, size_t(d.nc) * d.np, h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+int mprec_gpu_condensed_system(mprec_gpu_condensed* h, mprec_gpu_system** out) {
+    return guard([&] {
+        if (!h || !out) throw Error(MPREC_DIMENSION, "null argument");
+        const Condensed& d = h->cd;
+        if (d.np < 2) throw Error(MPREC_DIMENSION, "the reduced system needs P and T per cell");
+        auto s = std::make_unique<mprec_gpu_system>();
+        Pattern& p = s->pat;
+        p.nc = d.pat.nc;
+        p.nnzb = d.pat.nnzb;
+        p.h_rp = d.pat.h_rp;
+        p.h_ci = d.pat.h_ci;
+        p.h_dpos = d.pat.h_dpos;
+        p.rp.upload(p.h_rp.data(), p.h_rp.size(), s->ctx.s);
+        p.ci.upload(p.h_ci.data(), p.h_ci.size(), s->ctx.s);
+        p.dpos.upload(p.h_dpos.data(), p.h_dpos.size(), s->ctx.s);
+        const size_t nv = size_t(d.pat.nnzb) * d.np * d.np;
+        s->a_val.alloc(nv);
+        h->ctx.sync();
+        MG_CUDA(cudaMemcpyAsync(s->a_val.p, d.a_val.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, s->ctx.s));
+        s->nb = d.np;
+        s->n = int64_t(d.nc) * d.np;
+        s->b_host = d.b.to_host(h->ctx.s, size_t(s->n));
+        s->ctx.sync();
+        *out = s.release();
+    });
+}
+
+int mprec_gpu_back_substitute(mprec_gpu_condensed* h, const double* d1, double* d2) {
+    return guard([&] {
+        if (!h || !d1 || (!d2 && h->cd.n2 > 0)) throw Error(MPREC_DIMENSION, "null argument");
+        const Condensed& d = h->cd;
+        DBuf<double> x1(size_t(d.nc) * d.np), x2(size_t(std::max(d.n2, 1)));
+        x1.upload(d1, size_t(d.nc) * d.np, h->ctx.s);
+        back_substitute(h->ctx, d, x1.p, x2.p);
+        x2.download(d2, size_t(d.n2), h->ctx.s);
+        h->ctx.sync();
+    });
+}
+
+void mprec_gpu_condensed_destroy(mprec_gpu_condensed* h) { delete h; }
 
 int mprec_gpu_get_shape(mprec_gpu_system* h, int* n_cells, int* nb, int* nnzb) {
     return guard([&] {
