@@ -244,3 +244,155 @@ def mixed_states(n: int, seed: int) -> list:
     """A deterministic mix of G / OG / OWG cells (acceptance.cpp: mixed_states)."""
     rng = np.random.default_rng(seed)
     return [STATES[int(k)] for k in rng.integers(0, 3, size=n)]
+
+
+class PackedGlobalJacobian:
+    """A GlobalJacobian already in the C ABI's packed column-major arrays
+    (for large systems; see make_synthetic_global_bulk)."""
+
+    def __init__(self, n_cells, np_, row_ptr, col_idx, j11, sec_off, j22, j21, e_row, e_col, j12, r1, r2):
+        self.n_cells, self.np = int(n_cells), int(np_)
+        a32 = lambda a: np.ascontiguousarray(a, np.int32)  # noqa: E731
+        f64 = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
+        self.row_ptr, self.col_idx, self.sec_off = a32(row_ptr), a32(col_idx), a32(sec_off)
+        self.e_row, self.e_col = a32(e_row), a32(e_col)
+        self.j11, self.j22, self.j21, self.j12, self.r1, self.r2 = map(f64, (j11, j22, j21, j12, r1, r2))
+
+    @property
+    def n_secondary_total(self) -> int:
+        return int(self.sec_off[-1])
+
+    def bytes(self) -> int:
+        return sum(a.nbytes for a in (self.row_ptr, self.col_idx, self.sec_off, self.e_row, self.e_col, self.j11,
+                                      self.j22, self.j21, self.j12, self.r1, self.r2))
+
+    def c_struct(self) -> _GJ:
+        p = lambda a: a.ctypes.data  # noqa: E731
+        return _GJ(self.n_cells, self.np, p(self.row_ptr), p(self.col_idx), p(self.j11), p(self.sec_off),
+                   p(self.j22), p(self.j21), int(self.e_row.size), p(self.e_row), p(self.e_col), p(self.j12),
+                   p(self.r1), p(self.r2))
+
+
+def _cell_template(vp: VariablePartition):
+    """Structural pattern of make_cell_secondary_blocks for one phase state:
+    (j22 off-diagonal mask, j21 mask)."""
+    ns, np_ = vp.n_secondary, vp.n_primary
+    prim = vp.canonical_labels()
+    p_col, t_col = prim.index((PRESSURE, 0)), prim.index((TEMPERATURE, 0))
+    m22, m21 = np.zeros((ns, ns), bool), np.zeros((ns, np_), bool)
+    for r in range(ns):
+        kind, _ = vp.equations[r]
+        if kind == FUGACITY:
+            other = _counterpart(vp.secondary[r])
+            if other in vp.secondary:
+                m22[r, vp.secondary.index(other)] = True
+            if other in prim:
+                m21[r, prim.index(other)] = True
+            m21[r, p_col] = m21[r, t_col] = True
+        else:
+            phase = VAPOR_FRAC if kind == GAS_CONSTRAINT else OIL_FRAC
+            for c in range(ns):
+                if c != r and vp.secondary[c][0] == phase:
+                    m22[r, c] = True
+            for c in range(np_):
+                if prim[c][0] == phase:
+                    m21[r, c] = True
+    return m22, m21
+
+
+def make_synthetic_global_bulk(states, n_c: int, n_s: int, seed: int) -> PackedGlobalJacobian:
+    """make_synthetic_global's structure (1-D chain with inter-cell coupling),
+    vectorised per phase state, packed for the C ABI directly."""
+    rng = np.random.default_rng(seed)
+    st = np.asarray([STATES.index(s) if isinstance(s, str) else int(s) for s in states], np.int64)
+    nc = st.size
+    np_ = n_c + n_s + 1
+    parts = [ordering_for(s, n_c, n_s) for s in STATES]
+    ns_of = np.array([p.n_secondary for p in parts])[st]
+    sec_off = np.zeros(nc + 1, np.int64)
+    sec_off[1:] = np.cumsum(ns_of)
+    # J11: 1-D chain, blocks (c, c-1), (c, c), (c, c+1); column-major blocks
+    hi = 0.3 * _signed(rng, (max(nc - 1, 0), np_, np_))
+    lo = 0.3 * _signed(rng, (max(nc - 1, 0), np_, np_))
+    d = _signed(rng, (nc, np_, np_))
+    idx = np.arange(np_)
+    d[:-1, idx, idx] += np.abs(hi).sum(axis=2)
+    d[1:, idx, idx] += np.abs(lo).sum(axis=2)
+    off = np.abs(d).sum(axis=2) - np.abs(d[:, idx, idx])
+    dd = d[:, idx, idx]
+    d[:, idx, idx] = off + dd + np.where(dd >= 0.0, 1.0, -1.0) * rng.uniform(0.5, 2.0, (nc, np_))
+    cnt = np.full(nc, 3)
+    cnt[0] -= 1
+    cnt[-1] -= 1
+    if nc == 1:
+        cnt[0] = 1
+    row_ptr = np.zeros(nc + 1, np.int64)
+    row_ptr[1:] = np.cumsum(cnt)
+    nnzb = int(row_ptr[-1])
+    col_idx = np.empty(nnzb, np.int64)
+    j11 = np.empty((nnzb, np_, np_))
+    cells = np.arange(nc)
+    first = row_ptr[:-1]
+    has_lo = cells > 0
+    # positions: lo block (c, c-1) first, then diag, then hi (c, c+1)
+    lo_pos = first[has_lo]
+    col_idx[lo_pos] = cells[has_lo] - 1
+    j11[lo_pos] = lo
+    dpos = first + has_lo
+    col_idx[dpos] = cells
+    j11[dpos] = d
+    has_hi = cells < nc - 1
+    hi_pos = dpos[has_hi] + 1
+    col_idx[hi_pos] = cells[has_hi] + 1
+    j11[hi_pos] = hi
+    j11 = np.ascontiguousarray(j11.transpose(0, 2, 1)).reshape(-1)
+    # per-cell secondary blocks, by state
+    n22 = np.zeros(nc + 1, np.int64)
+    n22[1:] = np.cumsum(ns_of * ns_of)
+    j22 = np.zeros(int(n22[-1]))
+    j21 = np.zeros(int(sec_off[-1]) * np_)
+    own = np.zeros(int(sec_off[-1]) * np_)
+    for s_id, vp in enumerate(parts):
+        cs = np.nonzero(st == s_id)[0]
+        if cs.size == 0:
+            continue
+        ns = vp.n_secondary
+        m22, m21 = _cell_template(vp)
+        a22 = np.where(m22, _signed(rng, (cs.size, ns, ns)), 0.0)
+        a21 = np.where(m21, _signed(rng, (cs.size, ns, np_)), 0.0)
+        di = np.arange(ns)
+        a22[:, di, di] = np.abs(a22).sum(axis=2) + np.abs(a21).sum(axis=2) + rng.uniform(0.5, 2.0, (cs.size, ns))
+        pos22 = n22[cs][:, None] + np.arange(ns * ns)[None, :]
+        j22[pos22] = a22.transpose(0, 2, 1).reshape(cs.size, -1)
+        pos21 = (sec_off[cs] * np_)[:, None] + np.arange(ns * np_)[None, :]
+        j21[pos21] = a21.transpose(0, 2, 1).reshape(cs.size, -1)
+        o = 0.1 * _signed(rng, (cs.size, np_, ns))
+        own[pos21] = o.transpose(0, 2, 1).reshape(cs.size, -1)
+    # J12 list: (c, c) own, then (c, c+1) neighbour (np x ns_{c+1})
+    e_row = np.repeat(cells, 1 + has_hi)
+    e_col = e_row.copy()
+    nb_first = np.zeros(nc, np.int64)
+    nb_first[1:] = np.cumsum(1 + has_hi)[:-1]
+    e_col[nb_first[has_hi] + 1] = cells[has_hi] + 1
+    e_ns = ns_of[e_col]
+    e_off = np.zeros(e_row.size + 1, np.int64)
+    e_off[1:] = np.cumsum(e_ns * np_)
+    j12 = np.zeros(int(e_off[-1]))
+    own_e = nb_first
+    # own blocks: copy from `own` (np x ns_c column-major == the same packing)
+    for s_id, vp in enumerate(parts):
+        cs = np.nonzero(st == s_id)[0]
+        if cs.size == 0:
+            continue
+        ln = vp.n_secondary * np_
+        src = (sec_off[cs] * np_)[:, None] + np.arange(ln)[None, :]
+        dst = e_off[own_e[cs]][:, None] + np.arange(ln)[None, :]
+        j12[dst] = own[src]
+        # neighbour blocks pointing at cells of this state
+        nbc = cs[cs > 0]  # column cell of the (c-1, c) neighbour entry
+        if nbc.size:
+            dst = e_off[nb_first[nbc - 1] + 1][:, None] + np.arange(ln)[None, :]
+            j12[dst] = 0.05 * _signed(rng, (nbc.size, ln))
+    r2 = rng.uniform(-1.0, 1.0, int(sec_off[-1]))
+    r1 = rng.uniform(-1.0, 1.0, nc * np_)
+    return PackedGlobalJacobian(nc, np_, row_ptr, col_idx, j11, sec_off, j22, j21, e_row, e_col, j12, r1, r2)

@@ -16,6 +16,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "condense.cuh"
@@ -311,6 +312,8 @@ void condense(Ctx& c, const mprec_global_jacobian& j, Condensed& out) {
         for (int e = 0; e < ne; ++e) rlist[fill[er[e]]++] = e;
     }
 
+    Trace tr_all(&c, "condense total");
+    std::unique_ptr<Trace> tr(new Trace(&c, "condense H2D"));
     out.nc = nc;
     out.np = np;
     out.n2 = n2;
@@ -324,6 +327,17 @@ void condense(Ctx& c, const mprec_global_jacobian& j, Condensed& out) {
     DBuf<double> j22(size_t(std::max<int64_t>(luo[nc], 1)));
     if (luo[nc]) j22.upload(j.j22, size_t(luo[nc]), c.s);
     DBuf<double> x(size_t(std::max<int64_t>(int64_t(n2) * (np + 1), 1)));
+    DBuf<int> rp(nc + 1), ci11(std::max(nnzb, 1));
+    rp.upload(j.row_ptr, nc + 1, c.s);
+    ci11.upload(j.col_idx, nnzb, c.s);
+    DBuf<double> j11(size_t(nnzb) * np * np);
+    j11.upload(j.j11, size_t(nnzb) * np * np, c.s);
+    const int64_t j12n = eoff_all[j.n_j12];
+    DBuf<double> j12d(size_t(std::max<int64_t>(j12n, 1)));
+    if (j12n) j12d.upload(j.j12, size_t(j12n), c.s);
+    DBuf<double> r1(size_t(nc) * np);
+    r1.upload(j.r1, size_t(nc) * np, c.s);
+    tr.reset(new Trace(&c, "condense J22 LU + solves"));
     int* err = c.counters.p + 10;
     const int big = 0x7fffffff;
     MG_CUDA(cudaMemcpyAsync(err, &big, sizeof(int), cudaMemcpyHostToDevice, c.s));
@@ -339,12 +353,11 @@ void condense(Ctx& c, const mprec_global_jacobian& j, Condensed& out) {
     if (bad != big) throw Error(MPREC_SINGULAR_BLOCK, "singular secondary block", bad);
 
     // J12 products
-    const int64_t j12n = eoff_all[j.n_j12];
-    DBuf<double> j12d(size_t(std::max<int64_t>(j12n, 1))), corr(size_t(std::max<int64_t>(int64_t(ne) * np * np, 1))),
+    tr.reset(new Trace(&c, "condense J12 products"));
+    DBuf<double> corr(size_t(std::max<int64_t>(int64_t(ne) * np * np, 1))),
         vrhs(size_t(std::max<int64_t>(int64_t(ne) * np, 1)));
     DBuf<int> d_ec(std::max(ne, 1)), d_er(std::max(ne, 1)), d_rrp(nc + 1), d_rlist(std::max(ne, 1));
     DBuf<int64_t> d_eoff(std::max(ne, 1));
-    if (j12n) j12d.upload(j.j12, size_t(j12n), c.s);
     if (ne) {
         d_ec.upload(ec.data(), ne, c.s);
         d_er.upload(er.data(), ne, c.s);
@@ -358,12 +371,8 @@ void condense(Ctx& c, const mprec_global_jacobian& j, Condensed& out) {
     d_rrp.upload(rrp.data(), nc + 1, c.s);
 
     // assembly of the entry list [J11 blocks..., C_e...] (BlockMatrix::assemble)
+    tr.reset(new Trace(&c, "condense assembly"));
     const int m = nnzb + ne;
-    DBuf<int> rp(nc + 1), ci11(std::max(nnzb, 1));
-    rp.upload(j.row_ptr, nc + 1, c.s);
-    ci11.upload(j.col_idx, nnzb, c.s);
-    DBuf<double> j11(size_t(nnzb) * np * np);
-    j11.upload(j.j11, size_t(nnzb) * np * np, c.s);
     DBuf<unsigned long long> key(m), skey(m);
     DBuf<int> id(m), sid(m), head(m), pos(m + 1);
     k_cond_keys<<<(m + 255) / 256, 256, 0, c.s>>>(rp.p, ci11.p, nc, nnzb, d_er.p, d_ec.p, ne, key.p, id.p);
@@ -406,8 +415,6 @@ void condense(Ctx& c, const mprec_global_jacobian& j, Condensed& out) {
                                                                            corr.p, out.a_val.p);
         check_launch("condense merge");
     }
-    DBuf<double> r1(size_t(nc) * np);
-    r1.upload(j.r1, size_t(nc) * np, c.s);
     out.b.alloc(size_t(nc) * np);
     k_cond_rhs<<<int((int64_t(nc) * np + 255) / 256), 256, 0, c.s>>>(r1.p, d_rrp.p, d_rlist.p, vrhs.p, nc, np, out.b.p);
     check_launch("condense rhs");
@@ -420,6 +427,7 @@ void condense(Ctx& c, const mprec_global_jacobian& j, Condensed& out) {
         for (int k = out.pat.h_rp[r]; k < out.pat.h_rp[r + 1]; ++k)
             if (out.pat.h_ci[k] == r) out.pat.h_dpos[r] = k;
     out.pat.dpos.upload(out.pat.h_dpos.data(), nc, c.s);
+    tr.reset();
     c.sync();
 }
 
