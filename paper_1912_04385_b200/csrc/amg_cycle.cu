@@ -292,6 +292,9 @@ static void level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold
         gs_band_sweep(c, bs, L.a.nnz, L.n, r, zero ? nullptr : xold, xnew);
     else if (L.seg)
         gs_sweep_seg(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.seg_fwd : L.seg_bwd);
+    else if (L.cl_size > 0)
+        gs_sweep_cluster(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.border_f.p : L.border_b.p,
+                         L.cl_size, L.cl_R);
     else if (L.cta_B > 0)
         gs_sweep_cta(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.border_f.p : L.border_b.p, L.cta_B);
     else
@@ -384,7 +387,8 @@ void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int
 namespace mg {
 // Setup-time choice of the sweep kernel for one level (measure, don't guess):
 // row-per-warp (cross-SM hops), CTA bands of 4096 / 8192 rows (on-SM hops) or
-// band-segment chains (gs_seg.cu).  MPREC_GS_MODE forces one: warp | cta | seg.
+// band-segment chains (gs_seg.cu) or a whole level in one thread block cluster
+// (gs_cluster.cu).  MPREC_GS_MODE forces one: warp | cta | seg | cluster.
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     L.cta_B = 0;
     L.seg = false;
@@ -392,12 +396,25 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         const char* e = getenv("MPREC_GS_MODE");
         return std::string(e ? e : "");
     }();
+    L.cl_size = 0;
     if (force == "warp") return;
     // candidates by size (B200 measurements): the band kernels only
-    // win on the finest, million-row levels; below that no timing is needed
+    // win on the finest, million-row levels; the cluster kernel needs the whole
+    // level's iterate in one cluster's shared memory
     const bool try_cta = !force.empty() || L.n >= (1 << 20);
     const bool try_seg = !force.empty() || L.n >= (2 << 20);
-    if (force.empty() && !try_cta && !try_seg) return;
+    int cl_R = 0;
+    const int cl_size = gs_cluster_plan(L.n, &cl_R);
+    const bool try_cl = cl_size > 0 && (force.empty() || force == "cluster");
+    if (force == "cluster") {
+        if (!try_cl) return;
+        L.cl_size = cl_size;
+        L.cl_R = cl_R;
+        build_band_order(c, L.n, sf.level.p, cl_R, L.border_f);
+        build_band_order(c, L.n, sb.level.p, cl_R, L.border_b);
+        return;
+    }
+    if (force.empty() && !try_cta && !try_seg && !try_cl) return;
     const bool sorted = csr_sorted(c, L.a);
     if (force == "seg") {
         if (!sorted) return;
@@ -429,7 +446,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         }
         return best;
     };
-    const char* names[3] = {"row-per-warp", "cta-band", "band-segment"};
+    const char* names[4] = {"row-per-warp", "cta-band", "band-segment", "cluster"};
     int best_mode = 0, b_best = 0;
     float t_best = force.empty() ? time_fwd() : 1e30f;
     if ((force.empty() && try_cta) || force == "cta") {
@@ -462,6 +479,31 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         }
         L.seg = false;
     }
+    int cl_best = 0, cl_best_R = 0;
+    if (try_cl) {
+        // every feasible cluster size: more CTAs = more warps in flight, fewer local hops
+        for (int want : {1, 2, 4, 8, 16}) {
+            int r = 0;
+            const int cs = gs_cluster_plan(L.n, &r, want);
+            if (cs != want) continue;
+            L.cl_size = cs;
+            L.cl_R = r;
+            build_band_order(c, L.n, sf.level.p, r, L.border_f);
+            float t = 1e30f;
+            try {
+                t = time_fwd();
+            } catch (const Error&) {  // cluster not schedulable on this device
+                cudaGetLastError();
+            }
+            L.cl_size = 0;
+            if (t < t_best) {
+                t_best = t;
+                best_mode = 3;
+                cl_best = cs;
+                cl_best_R = r;
+            }
+        }
+    }
     if (best_mode != 2) {
         L.seg_fwd = SegSched();
         L.seg_bwd = SegSched();
@@ -475,6 +517,11 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     if (best_mode == 1) {
         build_band_order(c, L.n, sf.level.p, b_best, L.border_f);
         build_band_order(c, L.n, sb.level.p, b_best, L.border_b);
+    } else if (best_mode == 3) {
+        L.cl_size = cl_best;
+        L.cl_R = cl_best_R;
+        build_band_order(c, L.n, sf.level.p, cl_best_R, L.border_f);
+        build_band_order(c, L.n, sb.level.p, cl_best_R, L.border_b);
     } else {
         L.border_f.release();
         L.border_b.release();
@@ -483,6 +530,6 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     cudaEventDestroy(e1);
     if (trace_on())
         fprintf(stderr, "[mprec] level n=%d sweep: %s B=%d (%.3f ms fwd)\n", L.n, names[best_mode],
-                best_mode == 2 ? seg_best : L.cta_B, t_best);
+                best_mode == 2 ? seg_best : (best_mode == 3 ? L.cl_size : L.cta_B), t_best);
 }
 }  // namespace mg

@@ -946,9 +946,9 @@ static void coarse_factor(Ctx& c, const CsrView& a, DBuf<double>& lu, DBuf<doubl
         check_launch("dense lu");
     }
     // pivot check |u_ii| <= 1e-14 * max|a|
-    std::vector<double> h = lu.to_host(c.s, (size_t)n * n);
     double sc = 0.0;
-    MG_CUDA(cudaMemcpy(&sc, scale.p, sizeof(double), cudaMemcpyDeviceToHost));
+    scale.download(&sc, 1, c.s);
+    std::vector<double> h = lu.to_host(c.s, (size_t)n * n);  // synchronises c.s
     for (int i = 0; i < n; ++i)
         if (std::abs(h[(size_t)i * n + i]) <= 1e-14 * sc)
             throw Error(MPREC_SINGULAR_BLOCK, "singular dense-factor pivot block in cell " + std::to_string(i), i);

@@ -10,7 +10,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <functional>
+#include <thread>
 
 #include <cuda_profiler_api.h>
 
@@ -530,21 +532,58 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
             h->gE.ensure(2 * nc);
             h->xE.ensure(2 * nc);
         }
-        if (is_cptr3_method(method)) {
+        // The two stage hierarchies are independent (stages.cpp:129-138) and their
+        // setup is dominated by the sequential, single-warp RS first pass: build
+        // C_TT's on a second stream from a worker thread while B_PP's runs here.
+        const bool want_T = is_cptr3_method(method);
+        const bool want_P = method == MPREC_METHOD_CPR_AMG || method == MPREC_METHOD_CPR_DIRECT || want_T;
+        CsrView aT{}, aP{};
+        if (want_T) {
             h->fT.ensure(h->pat.nnzb);
             extract_field(c, h->Abar(), h->T(), h->fT.p);
-            CsrView a0{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fT.p, h->pat.dpos.p};
+            aT = CsrView{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fT.p, h->pat.dpos.p};
             h->amgT = std::make_unique<Amg>();
-            Trace tr(&c, "AMG(C_TT) setup total");
-            h->amgT->setup(c, a0, prm, &h->pat);
         }
-        if (method == MPREC_METHOD_CPR_AMG || method == MPREC_METHOD_CPR_DIRECT || is_cptr3_method(method)) {
+        if (want_P) {
             h->fP.ensure(h->pat.nnzb);
             extract_field(c, h->Abar(), h->P(), h->fP.p);
-            CsrView a0{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fP.p, h->pat.dpos.p};
+            aP = CsrView{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fP.p, h->pat.dpos.p};
             h->amgP = std::make_unique<Amg>();
+        }
+        if (want_T && want_P) {
+            h->pat.ensure_sched(c);  // shared, read-only from here on
+            c.sync();
+            Ctx c2;
+            std::exception_ptr err_T;
+            std::thread th([&] {
+                try {
+                    DeferFreeScope defer;  // no device-wide syncs from this thread's frees
+                    Trace tr(&c2, "AMG(C_TT) setup total");
+                    h->amgT->setup(c2, aT, prm, &h->pat);
+                    c2.sync();
+                } catch (...) {
+                    err_T = std::current_exception();
+                }
+            });
+            std::exception_ptr err_P;
+            try {
+                DeferFreeScope defer;
+                Trace tr(&c, "AMG(B_PP) setup total");
+                h->amgP->setup(c, aP, prm, &h->pat);
+                c.sync();
+            } catch (...) {
+                err_P = std::current_exception();
+            }
+            th.join();
+            // the reference builds C_TT first (stages.cpp:129-138): its error wins
+            if (err_T) std::rethrow_exception(err_T);
+            if (err_P) std::rethrow_exception(err_P);
+        } else if (want_T) {
+            Trace tr(&c, "AMG(C_TT) setup total");
+            h->amgT->setup(c, aT, prm, &h->pat);
+        } else if (want_P) {
             Trace tr(&c, "AMG(B_PP) setup total");
-            h->amgP->setup(c, a0, prm, &h->pat);
+            h->amgP->setup(c, aP, prm, &h->pat);
         }
         // ILU(0) of Ā
         h->lu_val.ensure(nv);

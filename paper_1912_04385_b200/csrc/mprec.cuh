@@ -174,6 +174,7 @@ struct AmgLevel {
     DBuf<double> invd;                // 1 / a_ii
     int cta_B = 0;                    // CTA-band sweep: rows per band (0: row-per-warp sweep)
     DBuf<int> border_f, border_b;     // band rows in global level order (fwd / bwd)
+    int cl_size = 0, cl_R = 0;        // cluster sweep (gs_cluster.cu): CTAs, rows per CTA
     bool seg = false;                 // segment-chain sweep (gs_seg.cu)
     SegSched seg_fwd, seg_bwd;        // segment bounds + claim orders (fwd / bwd)
 };
@@ -208,6 +209,9 @@ void build_band_order(Ctx& c, int n, const int* lev, int B, DBuf<int>& border);
 bool csr_sorted(Ctx& c, const CsrView& a);
 void build_seg_sched(Ctx& c, const CsrView& a, SegSched& fwd, SegSched& bwd);
 void build_seg_bands(Ctx& c, SegSched& seg, int B);
+int gs_cluster_plan(int n, int* rows_per_cta, int min_cs = 1);
+void gs_sweep_cluster(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
+                      int dir, bool xold_zero, const int* border, int csize, int R);
 void gs_sweep_seg(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
                   int dir, bool xold_zero, const SegSched& seg);
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb);

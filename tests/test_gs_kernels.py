@@ -26,7 +26,7 @@ def cfg2():
     return gen.generate(2)
 
 
-@pytest.mark.parametrize("mode", ["warp", "cta", "seg", ""])
+@pytest.mark.parametrize("mode", ["warp", "cta", "seg", "cluster", ""])
 @pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
 def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
     monkeypatch.setenv("MPREC_GS_MODE", mode)
