@@ -557,7 +557,7 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
             std::exception_ptr err_T;
             std::thread th([&] {
                 try {
-                    DeferFreeScope defer;  // no device-wide syncs from this thread's frees
+                    StreamAllocScope alloc_on(c2.s);  // no device-wide syncs from allocations
                     Trace tr(&c2, "AMG(C_TT) setup total");
                     h->amgT->setup(c2, aT, prm, &h->pat);
                     c2.sync();
@@ -567,7 +567,7 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
             });
             std::exception_ptr err_P;
             try {
-                DeferFreeScope defer;
+                StreamAllocScope alloc_on(c.s);
                 Trace tr(&c, "AMG(B_PP) setup total");
                 h->amgP->setup(c, aP, prm, &h->pat);
                 c.sync();

@@ -36,77 +36,43 @@ inline void check_launch(const char* what) {
     if (e != cudaSuccess) throw Error(MPREC_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// ---- deferred frees -----------------------------------------------------------
-// cudaFree synchronises the whole device.  While two host threads build
-// independent structures on two streams (the AMG hierarchies of one setup),
-// each thread parks the blocks it frees in a thread-local pool and reuses them
-// for its own later allocations (same thread = same stream, so stream order
-// makes the reuse safe); the pool is released when the scope ends.
-struct DeferredPool {
-    std::vector<std::pair<size_t, void*>> blocks;
+// ---- stream-ordered allocation scope -------------------------------------------
+// cudaMalloc / cudaFree may synchronise the whole device.  While two host
+// threads build independent structures on two streams (the AMG hierarchies of
+// one setup), each thread allocates and frees stream-ordered on its own stream
+// (cudaMallocAsync / cudaFreeAsync), so neither waits for the other's kernels.
+inline cudaStream_t& tl_alloc_stream() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+struct StreamAllocScope {
+    cudaStream_t prev;
+    explicit StreamAllocScope(cudaStream_t s) : prev(tl_alloc_stream()) { tl_alloc_stream() = s; }
+    ~StreamAllocScope() { tl_alloc_stream() = prev; }
 };
-inline DeferredPool*& tl_deferred_pool() {
-    static thread_local DeferredPool* p = nullptr;
-    return p;
-}
-struct DeferFreeScope {
-    DeferredPool pool;
-    DeferredPool* prev;
-    DeferFreeScope() : prev(tl_deferred_pool()) { tl_deferred_pool() = &pool; }
-    ~DeferFreeScope() {
-        tl_deferred_pool() = prev;
-        for (auto& b : pool.blocks) cudaFree(b.second);
-    }
-};
-// a parked block of at least `bytes` (smallest fit), or nullptr
-inline void* deferred_take(size_t bytes, size_t* cap) {
-    DeferredPool* p = tl_deferred_pool();
-    if (!p) return nullptr;
-    size_t best = size_t(-1);
-    int bi = -1;
-    for (int k = 0; k < int(p->blocks.size()); ++k)
-        if (p->blocks[k].first >= bytes && p->blocks[k].first < best && p->blocks[k].first <= 2 * bytes + (1 << 20)) {
-            best = p->blocks[k].first;
-            bi = k;
-        }
-    if (bi < 0) return nullptr;
-    void* ptr = p->blocks[bi].second;
-    *cap = p->blocks[bi].first;
-    p->blocks[bi] = p->blocks.back();
-    p->blocks.pop_back();
-    return ptr;
-}
-inline bool deferred_park(void* ptr, size_t cap) {
-    DeferredPool* p = tl_deferred_pool();
-    if (!p) return false;
-    p->blocks.emplace_back(cap, ptr);
-    return true;
-}
 
 // ---- device buffer ---------------------------------------------------------
 template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
-    size_t cap = 0;  // bytes of the underlying block
+    bool async_ = false;  // allocated stream-ordered (StreamAllocScope)
     DBuf() = default;
     explicit DBuf(size_t count) { alloc(count); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap) {
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), async_(o.async_) {
         o.p = nullptr;
         o.n = 0;
-        o.cap = 0;
     }
     DBuf& operator=(DBuf&& o) noexcept {
         if (this != &o) {
             release();
             p = o.p;
             n = o.n;
-            cap = o.cap;
+            async_ = o.async_;
             o.p = nullptr;
             o.n = 0;
-            o.cap = 0;
         }
         return *this;
     }
@@ -114,12 +80,12 @@ struct DBuf {
     void alloc(size_t count) {
         release();
         if (count) {
-            const size_t bytes = count * sizeof(T);
-            if (void* q = deferred_take(bytes, &cap)) {
-                p = static_cast<T*>(q);
+            if (cudaStream_t s = tl_alloc_stream()) {
+                MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+                async_ = true;
             } else {
-                MG_CUDA(cudaMalloc(&p, bytes));
-                cap = bytes;
+                MG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+                async_ = false;
             }
         }
         n = count;
@@ -128,10 +94,15 @@ struct DBuf {
         if (count > n) alloc(count);
     }
     void release() {
-        if (p && !deferred_park(p, cap)) cudaFree(p);
+        if (p) {
+            cudaStream_t s = tl_alloc_stream();
+            if (async_ && s)
+                cudaFreeAsync(p, s);
+            else
+                cudaFree(p);
+        }
         p = nullptr;
         n = 0;
-        cap = 0;
     }
     size_t bytes() const { return n * sizeof(T); }
     void upload(const T* h, size_t count, cudaStream_t s) {
