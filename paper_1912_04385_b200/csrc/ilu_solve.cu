@@ -30,7 +30,7 @@ constexpr int kWarps = 8;
 
 // ---- nb = 8: lane l -> (row r = l & 7, column pair cq = l >> 3 : c = 2cq, 2cq+1)
 template <bool kFwd>
-__global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp, const int* __restrict__ ci,
+__global__ void __launch_bounds__(kWarps * 32, 4) k_ilu8(const int* __restrict__ rp, const int* __restrict__ ci,
                                                       const int* __restrict__ dpos, const double* __restrict__ val,
                                                       const double* __restrict__ rhs, double* y, int nc,
                                                       const int* __restrict__ order, int* counter,
@@ -52,17 +52,20 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp
         double drow[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) drow[c] = __ldg(bd + c * 8 + r);
+        // also off the chain: the polls below are volatile asm with a memory
+        // clobber, so a load written after them could not be hoisted
+        const double rhs_r = rhs[(int64_t)I * 8 + r];
         double acc = 0.0;
-        // dependency blocks in groups of 4: block values first, then ALL polls
+        // dependency blocks in groups of 2 (64 registers, 4 CTAs/SM): block values first, then ALL polls
         // issued together, then a warp-convergent re-poll of the pending ones
-        for (int kk = ka; kk < kb; kk += 4) {
-            double va[4][2];
-            unsigned long long raw[4][2];
-            int K[4];
-            bool pend[4][2];
+        for (int kk = ka; kk < kb; kk += 2) {
+            double va[2][2];
+            unsigned long long raw[2][2];
+            int K[2];
+            bool pend[2][2];
             bool any = false;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 2; ++u) {
                 const bool ok = kk + u < kb;
                 K[u] = ok ? __ldg(ci + kk + u) : 0;
                 const double* bk = val + (int64_t)(ok ? kk + u : ka) * 64;
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp
                 pend[u][0] = pend[u][1] = ok;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 2; ++u)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     raw[u][h] = pend[u][h] ? ld_relaxed(y + (int64_t)K[u] * 8 + c0 + h) : 0ull;
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp
             while (__any_sync(0xffffffffu, any)) {
                 any = false;
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < 2; ++u)
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
                         if (pend[u][h]) {
@@ -91,19 +94,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu8(const int* __restrict__ rp
                         }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 2; ++u)
                 acc += va[u][0] * __longlong_as_double((long long)raw[u][0]) +
                        va[u][1] * __longlong_as_double((long long)raw[u][1]);
         }
         acc += __shfl_xor_sync(0xffffffffu, acc, 8);
         acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-        const double v = rhs[(int64_t)I * 8 + r] - acc;
+        const double v = rhs_r - acc;
         // y_I = inv(L_II) v (forward) or inv(U_II) v (backward): 8 independent
         // shuffles + FMAs instead of an 8-step serial substitution
         double yv[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) yv[c] = __shfl_sync(0xffffffffu, v, c);
-        double out = kFwd ? yv[r] : 0.0;
+        double out = kFwd ? v : 0.0;  // y_r itself (a dynamic yv[r] would live in local memory)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             if (kFwd ? (c < r) : (c >= r)) out += drow[c] * yv[c];
@@ -138,6 +141,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu_gen(const int* __restrict__
         const int d = dpos[I];
         const int ka = kFwd ? rp[I] : d + 1;
         const int kb = kFwd ? d : rp[I + 1];
+        const double rhs_l = lane < nb ? rhs[(int64_t)I * nb + lane] : 0.0;  // before the polls
         double acc = 0.0;
         for (int k = ka; k < kb; ++k) {
             const int K = __ldg(ci + k);
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_ilu_gen(const int* __restrict__
             }
         }
         const double* bd = val + (int64_t)d * nb2;
-        double v = lane < nb ? rhs[(int64_t)I * nb + lane] - acc : 0.0;
+        double v = lane < nb ? rhs_l - acc : 0.0;
         if (kFwd) {
             for (int c = 0; c < nb - 1; ++c) {
                 const double yc = __shfl_sync(0xffffffffu, v, c);
