@@ -288,7 +288,10 @@ void dense_gemv(Ctx& c, const double* m, int n, const double* x, double* y) {
 // one Gauss-Seidel direction on level L: band schedule when available
 static void level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold, double* xnew, int dir, bool zero) {
     const BandSched& bs = dir > 0 ? L.band_fwd : L.band_bwd;
-    if (bs.ok)
+    const LsSched& ls = dir > 0 ? L.ls_fwd : L.ls_bwd;
+    if (ls.ok)
+        gs_sweep_ls(c, L.a, L.invd.p, r, xold, xnew, zero, ls);
+    else if (bs.ok)
         gs_band_sweep(c, bs, L.a.nnz, L.n, r, zero ? nullptr : xold, xnew);
     else if (L.seg)
         gs_sweep_seg(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.seg_fwd : L.seg_bwd);
@@ -299,6 +302,10 @@ static void level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold
         gs_sweep_cta(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.border_f.p : L.border_b.p, L.cta_B);
     else
         gs_sweep(c, L.a, r, xold, xnew, dir, zero, dir > 0 ? L.ofwd : L.obwd, L.invd.p);
+}
+
+void gs_level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold, double* xnew, int dir, bool zero) {
+    level_sweep(c, L, r, xold, xnew, dir, zero);
 }
 
 // amg.cpp:216-231
@@ -392,12 +399,25 @@ namespace mg {
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     L.cta_B = 0;
     L.seg = false;
+    L.ls_fwd = LsSched();
+    L.ls_bwd = LsSched();
     const std::string force = [] {  // read per setup so tests can force each kernel
         const char* e = getenv("MPREC_GS_MODE");
         return std::string(e ? e : "");
     }();
     L.cl_size = 0;
     if (force == "warp") return;
+    if (force == "ls") {
+        if (!L.glev_f || !L.glev_b || !csr_sorted(c, L.a)) return;
+        const int K = [] {
+            const char* e = getenv("MPREC_GS_LS_K");
+            return e ? atoi(e) : 16;
+        }();
+        if (build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, L.ls_fwd))
+            build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, K, L.ls_bwd);
+        if (!L.ls_bwd.ok) L.ls_fwd = LsSched();
+        return;
+    }
     // candidates by size (B200 measurements): the band kernels only
     // win on the finest, million-row levels; the cluster kernel needs the whole
     // level's iterate in one cluster's shared memory
@@ -414,7 +434,8 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         build_band_order(c, L.n, sb.level.p, cl_R, L.border_b);
         return;
     }
-    if (force.empty() && !try_cta && !try_seg && !try_cl) return;
+    const bool try_ls = L.glev_f && L.glev_b && L.n >= 2048;
+    if (force.empty() && !try_cta && !try_seg && !try_cl && !try_ls) return;
     const bool sorted = csr_sorted(c, L.a);
     if (force == "seg") {
         if (!sorted) return;
@@ -446,7 +467,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         }
         return best;
     };
-    const char* names[4] = {"row-per-warp", "cta-band", "band-segment", "cluster"};
+    const char* names[5] = {"row-per-warp", "cta-band", "band-segment", "cluster", "level-sync"};
     int best_mode = 0, b_best = 0;
     float t_best = force.empty() ? time_fwd() : 1e30f;
     if ((force.empty() && try_cta) || force == "cta") {
@@ -504,6 +525,36 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
             }
         }
     }
+    // level-synchronous pipelined programs (gs_ls.cu): group counts by level size
+    // (B200 measurements: 74 groups win on million-row levels, fewer below)
+    int ls_K = 0;
+    if (try_ls && sorted) {
+        std::vector<int> cands;
+        if (L.n >= (1 << 20))
+            cands = {74};
+        else if (L.n >= 300000)
+            cands = {148, 74};
+        else if (L.n >= 50000)
+            cands = {74, 37};
+        else
+            cands = {37, 16};
+        for (int K : cands) {
+            L.ls_fwd = LsSched();
+            if (!build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, L.ls_fwd)) continue;
+            const float t = time_fwd();
+            if (t < t_best) {
+                t_best = t;
+                ls_K = K;
+            }
+        }
+        L.ls_fwd = LsSched();
+    }
+    if (ls_K > 0) {
+        best_mode = 4;
+        build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, ls_K, L.ls_fwd);
+        build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, ls_K, L.ls_bwd);
+        if (!L.ls_bwd.ok) L.ls_fwd = LsSched();  // both directions or neither
+    }
     if (best_mode != 2) {
         L.seg_fwd = SegSched();
         L.seg_bwd = SegSched();
@@ -530,6 +581,6 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     cudaEventDestroy(e1);
     if (trace_on())
         fprintf(stderr, "[mprec] level n=%d sweep: %s B=%d (%.3f ms fwd)\n", L.n, names[best_mode],
-                best_mode == 2 ? seg_best : (best_mode == 3 ? L.cl_size : L.cta_B), t_best);
+                best_mode == 2 ? seg_best : (best_mode == 3 ? L.cl_size : best_mode == 4 ? ls_K : L.cta_B), t_best);
 }
 }  // namespace mg

@@ -1003,11 +1003,15 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
                 pat->ensure_sched(c);
                 l.ofwd = pat->fwd.order.p;
                 l.obwd = pat->bwd.order.p;
+                l.glev_f = pat->fwd.level.p;
+                l.glev_b = pat->bwd.level.p;
             } else {
                 build_sched(c, l.n, l.a.rp, l.a.ci, +1, l.own_fwd);
                 build_sched(c, l.n, l.a.rp, l.a.ci, -1, l.own_bwd);
                 l.ofwd = l.own_fwd.order.p;
                 l.obwd = l.own_bwd.order.p;
+                l.glev_f = l.own_fwd.level.p;
+                l.glev_b = l.own_bwd.level.p;
             }
             l.invd.alloc(std::max(l.n, 1));
             compute_invd(c, l.a, l.invd.p);

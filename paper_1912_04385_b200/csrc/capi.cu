@@ -99,23 +99,23 @@ struct GmresOut {
     double final_true_residual = 0.0;
 };
 
-// Krylov basis allocated lazily in chunks (at c5 one vector is 256 MB).
+// Krylov basis allocated lazily in chunks of kBasisChunk vectors (at
+// c5 one vector is 256 MB), stored tile-major for the Gram passes (gram.cu).
 struct Basis {
     int64_t n = 0;
-    int chunk = 8;
     std::vector<DBuf<double>> blocks;
-    double* vec(int i) {
-        const int b = i / chunk;
-        while (int(blocks.size()) <= b) blocks.emplace_back(size_t(n) * chunk);
-        return blocks[b].p + int64_t(i % chunk) * n;
+    double* chunk(int c) {
+        while (int(blocks.size()) <= c) blocks.emplace_back(size_t(basis_chunk_doubles(n)));
+        return blocks[c].p;
     }
 };
 
 struct Krylov {
     Basis V;
-    DBuf<double> w, t, hcol, cre;
-    DBuf<const double*> vtab;
+    DBuf<double> w, t, vk, hcol, cre;
     DBuf<double> ydev;
+    DBuf<double*> ct;             // chunk pointer table
+    DBuf<double> gt, pbuf, part;  // transposed Gram lower part, coefficients, pass-A partials
 };
 
 // gmres.cpp:8-106 over device vectors.  b, x: device; n unknowns.
@@ -140,8 +140,15 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
     kr.t.ensure(n);
     kr.hcol.ensure(max_it + 2);
     kr.cre.ensure(max_it + 2);
+    kr.vk.ensure(n);
+    kr.ct.ensure(max_it / kBasisChunk + 2);
+    kr.gt.ensure(size_t(max_it + 1) * (max_it + 1));
+    kr.pbuf.ensure(max_it + 2);
+    kr.part.ensure(size_t(gram_part_size(c, max_it)));
     int* gate = c.err.p + 8;
-    div_scalar(c, kr.V.vec(0), b, bnorm, n);
+    gram_set_ptr(c, kr.ct.p, 0, kr.V.chunk(0));
+    basis_put(c, kr.V.chunk(0), 0, b, bnorm, n);
+    const double* const* ct = kr.ct.p;
     const int ld = max_it + 1;
     std::vector<double> h(size_t(ld) * std::max(max_it, 1), 0.0), cs(max_it), sn(max_it), g(max_it + 1, 0.0);
     auto H = [&](int i, int j) -> double& { return h[size_t(j) * ld + i]; };
@@ -150,24 +157,20 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
     std::vector<double> col(max_it + 4);
     int k = 0;
     for (; k < max_it; ++k) {
-        double* vk = kr.V.vec(k);
+        double* vk = kr.vk.p;
+        basis_get(c, vk, kr.V.chunk(k / kBasisChunk), k % kBasisChunk, n);
         M(vk, kr.t.p);
         A(kr.t.p, kr.w.p);
         double* w = kr.w.p;
         double* hc = kr.hcol.p;
         double* cr = kr.cre.p;
-        nrm2(c, w, n, sc + 1);
-        // MGS (gmres.cpp:39-42), axpy of step i fused with the dot of step i+1
-        mgs_step(c, w, nullptr, nullptr, kr.V.vec(0), n, hc + 0, false, nullptr, nullptr);
-        for (int i = 1; i <= k; ++i)
-            mgs_step(c, w, kr.V.vec(i - 1), hc + i - 1, kr.V.vec(i), n, hc + i, false, nullptr, nullptr);
-        mgs_step(c, w, vk, hc + k, w, n, sc + 2, false, nullptr, nullptr);  // w -= h_kk v_k ; ||w||
+        // MGS (gmres.cpp:39-42) in Gram form (gram.cu): V^T w and the basis' new
+        // Gram row in one pass, (I + L) h = V^T w, w -= V h in a second pass
+        gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, false, k > 0, sc + 1, sc + 2, kr.part.p, nullptr);
         // one re-orthogonalisation pass when ||w|| < 0.7 pre_norm (gmres.cpp:44-50), gated on device
         set_reorth_gate(c, sc + 2, sc + 1, gate);
-        mgs_step(c, w, nullptr, nullptr, kr.V.vec(0), n, cr + 0, true, hc + 0, gate);
-        for (int i = 1; i <= k; ++i)
-            mgs_step(c, w, kr.V.vec(i - 1), cr + i - 1, kr.V.vec(i), n, cr + i, true, hc + i, gate);
-        mgs_step(c, w, vk, cr + k, w, n, sc + 3, false, nullptr, gate);
+        gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, true, false, nullptr, sc + 3, kr.part.p, gate);
+        (void)cr;
         // read back the Hessenberg column
         MG_CUDA(cudaMemcpyAsync(col.data(), hc, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c.s));
         double tail[3];
@@ -206,7 +209,9 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
             ++k;
             break;
         }
-        div_scalar(c, kr.V.vec(k + 1), w, subdiag, n);
+        if ((k + 1) % kBasisChunk == 0)
+            gram_set_ptr(c, kr.ct.p, (k + 1) / kBasisChunk, kr.V.chunk((k + 1) / kBasisChunk));
+        basis_put(c, kr.V.chunk((k + 1) / kBasisChunk), (k + 1) % kBasisChunk, w, subdiag, n);
     }
     out.iterations = k;
     if (k > 0) {
@@ -216,13 +221,9 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
             for (int j = i + 1; j < k; ++j) acc -= H(i, j) * y[j];
             y[i] = acc / H(i, i);
         }
-        std::vector<const double*> tab(k);
-        for (int i = 0; i < k; ++i) tab[i] = kr.V.vec(i);
-        kr.vtab.ensure(k);
         kr.ydev.ensure(k);
-        kr.vtab.upload(tab.data(), k, c.s);
         kr.ydev.upload(y.data(), k, c.s);
-        multi_axpy(c, kr.w.p, kr.vtab.p, kr.ydev.p, k, n);
+        basis_combine(c, ct, k, kr.ydev.p, kr.w.p, n);
         M(kr.w.p, x);
         c.sync();  // the host vectors above must outlive the async uploads
     } else {
@@ -268,6 +269,7 @@ void write_system(const char* mtx, const char* layout, const char* rhs, int nc, 
                   const std::vector<int>& ci, const std::vector<double>& val, const double* b);
 void ilu_timeline(Ctx& c, Ilu& ilu, const double* r, double* y, long long* ts_dev, int blocks);
 void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int* nl_f, int* nl_b);
+void gs_ls_experiment(Ctx& c, Amg& amg, int l, int K, int reps, double* out);
 void gs_seg_timeline(Ctx& c, Amg& amg, int l, long long* host, int* nseg);
 void gs_band_timeline(Ctx& c, Amg& amg, int l, long long* host_ts, int* nbands);
 }
@@ -1053,6 +1055,16 @@ int mprec_gpu_debug_gs(mprec_gpu_system* h, int stage, int level, int reps, doub
             *nl_f = h->pat.fwd.nlev;
             *nl_b = h->pat.bwd.nlev;
         }
+    });
+}
+
+// Diagnostics: level-synchronous sweep programs with K groups on one level vs the current kernel.
+int mprec_gpu_debug_gs_ls(mprec_gpu_system* h, int stage, int level, int K, int reps, double* out10) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        Amg* a = (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) ? h->amgT.get() : h->amgP.get();
+        if (!a || level < 0 || level + 1 >= a->n_levels()) throw Error(MPREC_INDEX, "level out of range");
+        gs_ls_experiment(h->ctx, *a, level, K, reps, out10);
     });
 }
 

@@ -1,0 +1,337 @@
+// gram.cu -- Arnoldi orthogonalisation of gmres.cpp:39-50 in Gram (inverse
+// compact WY) form: two passes over the Krylov basis per MGS sweep instead of
+// one fused dot/axpy pass per basis vector.
+//
+// Modified Gram-Schmidt computes, for i = 0..k in order,
+//     h_i = <w - sum_{j<i} h_j v_j, v_i> = <w, v_i> - sum_{j<i} G_ij h_j,
+// with G_ij = <v_j, v_i>, i.e. (I + L) h = V^T w where L is the strictly lower
+// part of the Gram matrix of the basis -- exactly, for any basis, not only an
+// orthogonal one.  So one sweep is
+//     pass A   p = V^T w            (one read of the basis, all dots at once)
+//     solve    (I + L) h = p        (k^2/2 flops, one thread block)
+//     pass B   w <- w - sum_i h_i v_i  (one read of the basis; per element the
+//                                      updates are applied in i order, as MGS)
+// and the new row of G (<v_j, v_k>, j < k) is computed in the same pass A as
+// the dots with w, reading the basis once.  The reference's re-orthogonalisation
+// (a second sweep when ||w|| < 0.7 ||w_0||, h += c) is the same three steps gated
+// on a device flag.  Traffic per sweep: 16 n (k + 1) bytes + O(n) instead of
+// 32 n (k + 1) for the fused per-vector MGS kernel, and 4 launches instead of
+// k + 2.  Results differ from the sequential sweep only by rounding (same
+// loss-of-orthogonality class as MGS; GMRES iteration counts stay within the
+// reference's +-1 bar, tests/test_gpu_parity.py).
+#include "mprec.cuh"
+
+namespace mg {
+namespace {
+
+constexpr int kGT = 256;             // threads per block
+constexpr int kT = kBasisTile;       // rows per tile (basis storage tile)
+constexpr int kGV = kBasisChunk;     // basis vectors per storage chunk
+constexpr int kGRed = 2 * kGV + 1;
+constexpr int kRPT = kT / kGT;       // rows per thread per tile
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Basis storage (capi.cu: Basis): chunk c holds vectors 8c..8c+7 tile-major,
+// [tile][8][kT]: the 8 vectors' rows of one tile are one contiguous 128 KB
+// region, so both passes stream long contiguous runs (DRAM row-buffer friendly)
+// instead of k + 1 interleaved vector streams.
+__device__ __forceinline__ const double* tile_base(const double* const* ct, int c, int64_t tile) {
+    return ct[c] + tile * (int64_t(kGV) * kT);
+}
+
+// Per-block partial sums of p_i = <v_i, w> (i <= k), q_j = <v_j, v_k> (j < k)
+// and <w, w>, over a fixed set of tiles (tile = blockIdx.x + t * gridDim.x):
+// part[blk * stride + {0..k | k+1..2k+1 | 2k+2}].
+__global__ void __launch_bounds__(kGT) k_gram_a(const double* const* __restrict__ ct, int k,
+                                                 const double* __restrict__ w, int64_t n, double* __restrict__ part,
+                                                 int stride, int want_q, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;
+    extern __shared__ double sm[];
+    double* acc = sm;
+    double* red = acc + stride;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < stride; i += kGT) acc[i] = 0.0;
+    const int64_t ntiles = (n + kT - 1) / kT;
+    const int ck = k / kGV, jk = k % kGV;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * kT;
+        const int nr = int(n - r0 < kT ? n - r0 : kT);
+        double wr[kRPT], vr[kRPT];
+        const double* vkp = tile_base(ct, ck, tile) + jk * kT;
+#pragma unroll
+        for (int q = 0; q < kRPT; ++q) {
+            const int r = tid + q * kGT;
+            wr[q] = r < nr ? w[r0 + r] : 0.0;
+            vr[q] = (r < nr && want_q) ? vkp[r] : 0.0;
+        }
+        for (int c = 0; c <= ck; ++c) {
+            const double* base = tile_base(ct, c, tile);
+            const int nv = c < ck ? kGV : jk + 1;
+            double ap[kGV], aq[kGV], aw = 0.0;
+#pragma unroll
+            for (int j = 0; j < kGV; ++j) {
+                ap[j] = aq[j] = 0.0;
+                if (j < nv) {
+#pragma unroll
+                    for (int q = 0; q < kRPT; ++q) {
+                        const int r = tid + q * kGT;
+                        const double x = r < nr ? __ldcs(base + j * kT + r) : 0.0;
+                        ap[j] += x * wr[q];
+                        aq[j] += x * vr[q];
+                    }
+                }
+            }
+            if (c == 0)
+#pragma unroll
+                for (int q = 0; q < kRPT; ++q) aw += wr[q] * wr[q];
+#pragma unroll
+            for (int j = 0; j < kGV; ++j) {
+                ap[j] = warp_sum(ap[j]);
+                aq[j] = warp_sum(aq[j]);
+            }
+            aw = warp_sum(aw);
+            __syncthreads();  // previous chunk's red consumed
+            if (lane == 0) {
+#pragma unroll
+                for (int j = 0; j < kGV; ++j) {
+                    red[wid * kGRed + j] = ap[j];
+                    red[wid * kGRed + kGV + j] = aq[j];
+                }
+                red[wid * kGRed + 2 * kGV] = aw;
+            }
+            __syncthreads();
+            if (tid < kGRed) {
+                double s = 0.0;
+                for (int q = 0; q < kGT / 32; ++q) s += red[q * kGRed + tid];
+                if (tid < kGV) {
+                    if (tid < nv) acc[c * kGV + tid] += s;
+                } else if (tid < 2 * kGV) {
+                    const int j = c * kGV + tid - kGV;
+                    if (j < k) acc[k + 1 + j] += s;
+                } else if (c == 0) {
+                    acc[2 * k + 2] += s;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < stride; i += kGT) part[int64_t(blockIdx.x) * stride + i] = acc[i];
+}
+
+// Sum the per-block partials in block order; scatter p, the new Gram row (stored
+// transposed: gt[j * ld + k] = <v_j, v_k>) and sqrt(<w, w>).
+__global__ void k_gram_fin(const double* __restrict__ part, int nblk, int stride, int k, double* p_out, double* gt,
+                           int ld, double* norm_out, int want_q, const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;
+    // one warp per output: lane l sums blocks l, l + 32, ... then a fixed shuffle tree
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (i >= stride) return;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += part[int64_t(b) * stride + i];
+    s = warp_sum(s);
+    if (lane != 0) return;
+    if (i <= k)
+        p_out[i] = s;
+    else if (i <= 2 * k + 1) {
+        const int j = i - (k + 1);
+        if (want_q && j < k) gt[int64_t(j) * ld + k] = s;
+    } else if (norm_out) {
+        *norm_out = sqrt(s);
+    }
+}
+
+// (I + L) c = p by forward substitution, column by column (h_i accumulates its
+// corrections in j order); c overwrites p, h = c or h += c (re-orthogonalisation).
+__global__ void k_gram_tri(const double* __restrict__ gt, int ld, int k, double* p, double* h, int accumulate,
+                           const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;
+    extern __shared__ double ps[];
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) ps[i] = p[i];
+    __syncthreads();
+    for (int j = 0; j < k; ++j) {
+        const double hj = ps[j];
+        const double* col = gt + int64_t(j) * ld;
+        for (int i = j + 1 + threadIdx.x; i <= k; i += blockDim.x) ps[i] -= col[i] * hj;
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+        p[i] = ps[i];
+        h[i] = accumulate ? h[i] + ps[i] : ps[i];
+    }
+}
+
+// mode 0: w <- w - sum_{i<=k} c_i v_i (per element in i order), norm_out =
+// ||w||; mode 1: w <- sum_{i<=k} c_i v_i (GMRES solution update, no norm).
+// Tile-major: each thread keeps its kRPT rows of the tile in registers while the
+// basis chunks of the tile stream by.
+__global__ void __launch_bounds__(kGT) k_gram_b(const double* const* __restrict__ ct, int k,
+                                                 const double* __restrict__ cvec, double* __restrict__ w, int64_t n,
+                                                 double* partials, unsigned* ctr, double* norm_out, int mode,
+                                                 const int* __restrict__ gate) {
+    if (gate && *gate == 0) return;
+    extern __shared__ double sm[];
+    double* cs = sm;
+    double* red = cs + k + 1;
+    for (int i = threadIdx.x; i <= k; i += kGT) cs[i] = cvec[i];
+    __syncthreads();
+    const int64_t ntiles = (n + kT - 1) / kT;
+    const int ck = k / kGV, jk = k % kGV;
+    double ss = 0.0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * kT;
+        const int nr = int(n - r0 < kT ? n - r0 : kT);
+        double x[kRPT];
+#pragma unroll
+        for (int q = 0; q < kRPT; ++q) {
+            const int r = threadIdx.x + q * kGT;
+            x[q] = (mode == 0 && r < nr) ? w[r0 + r] : 0.0;
+        }
+        for (int c = 0; c <= ck; ++c) {
+            const double* base = tile_base(ct, c, tile);
+            const int nv = c < ck ? kGV : jk + 1;
+#pragma unroll
+            for (int j = 0; j < kGV; ++j)
+                if (j < nv) {
+                    const double cj = cs[c * kGV + j];
+#pragma unroll
+                    for (int q = 0; q < kRPT; ++q) {
+                        const int r = threadIdx.x + q * kGT;
+                        const double v = r < nr ? __ldcs(base + j * kT + r) : 0.0;
+                        if (mode == 0)
+                            x[q] -= cj * v;
+                        else
+                            x[q] += cj * v;
+                    }
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < kRPT; ++q) {
+            const int r = threadIdx.x + q * kGT;
+            if (r < nr) {
+                w[r0 + r] = x[q];
+                ss += x[q] * x[q];
+            }
+        }
+    }
+    if (mode != 0) return;
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int q = 0; q < kGT / 32; ++q) s += red[q];
+        partials[blockIdx.x] = s;
+        __threadfence();
+        last = atomicInc(ctr, 0xFFFFFFFFu) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    double s = 0.0;
+    for (int b = 0; b < int(gridDim.x); ++b) s += reinterpret_cast<volatile double*>(partials)[b];
+    *norm_out = sqrt(s);
+    *ctr = 0;
+}
+
+__global__ void k_set_ptr(double** tab, int i, double* p) { tab[i] = p; }
+
+// vector j of a chunk <- x / a (put) or y <- vector j of a chunk (get)
+__global__ void k_basis_put(double* chunk, int j, const double* __restrict__ x, double a, int64_t n) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x)
+        chunk[(r / kT) * (int64_t(kGV) * kT) + j * kT + (r % kT)] = x[r] / a;
+}
+__global__ void k_basis_get(double* y, const double* __restrict__ chunk, int j, int64_t n) {
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x)
+        y[r] = chunk[(r / kT) * (int64_t(kGV) * kT) + j * kT + (r % kT)];
+}
+
+inline int tile_grid(Ctx& c, int64_t n, int per_sm) {
+    const int64_t ntiles = (n + kT - 1) / kT;
+    return int(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(per_sm) * c.sm_count)));
+}
+
+}  // namespace
+
+int64_t basis_chunk_doubles(int64_t n) { return ((n + kT - 1) / kT) * int64_t(kGV) * kT; }
+
+void gram_set_ptr(Ctx& c, double** tab, int i, double* p) {
+    k_set_ptr<<<1, 1, 0, c.s>>>(tab, i, p);
+    check_launch("gram ptr");
+}
+
+void basis_put(Ctx& c, double* chunk, int j, const double* x, double a, int64_t n) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * n);
+    k_basis_put<<<grid_for(n, 256), 256, 0, c.s>>>(chunk, j, x, a, n);
+    check_launch("basis put");
+}
+
+void basis_get(Ctx& c, double* y, const double* chunk, int j, int64_t n) {
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * n);
+    k_basis_get<<<grid_for(n, 256), 256, 0, c.s>>>(y, chunk, j, n);
+    check_launch("basis get");
+}
+
+int gram_part_size(Ctx& c, int kmax) { return 4 * c.sm_count * (2 * (kmax + 1) + 1); }
+
+void gram_sweep(Ctx& c, const double* const* ct, int k, double* w, int64_t n, double* gt, int ld, double* pbuf,
+                double* h, bool accumulate, bool want_q, double* pre_norm, double* post_norm, double* part,
+                const int* gate) {
+    const int stride = 2 * (k + 1) + 1;
+    const int grid_a = tile_grid(c, n, 4);
+    {
+        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 2));
+        const size_t smem = sizeof(double) * (stride + (kGT / 32) * kGRed);
+        static size_t attr = 0;
+        if (smem > 48 * 1024 && smem > attr) {
+            MG_CUDA(cudaFuncSetAttribute(k_gram_a, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr = smem;
+        }
+        k_gram_a<<<grid_a, kGT, smem, c.s>>>(ct, k, w, n, part, stride, want_q ? 1 : 0, gate);
+        check_launch("gram pass A");
+    }
+    {
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * grid_a * stride);
+        k_gram_fin<<<(stride + 7) / 8, 256, 0, c.s>>>(part, grid_a, stride, k, pbuf, gt, ld, pre_norm,
+                                                      want_q ? 1 : 0, gate);
+        check_launch("gram fin");
+    }
+    {
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * (k + 1) * (k + 1) / 2);
+        k_gram_tri<<<1, 512, sizeof(double) * (k + 1), c.s>>>(gt, ld, k, pbuf, h, accumulate ? 1 : 0, gate);
+        check_launch("gram tri");
+    }
+    {
+        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 3));
+        const size_t smem = sizeof(double) * (k + 1 + kGT / 32);
+        static size_t attr = 0;
+        if (smem > 48 * 1024 && smem > attr) {
+            MG_CUDA(cudaFuncSetAttribute(k_gram_b, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr = smem;
+        }
+        const int grid_b = std::min(tile_grid(c, n, 8), kRedBlocks);
+        k_gram_b<<<grid_b, kGT, smem, c.s>>>(ct, k, pbuf, w, n, c.red.p, c.red_ctr.p + 8, post_norm, 0, gate);
+        check_launch("gram pass B");
+    }
+}
+
+void basis_combine(Ctx& c, const double* const* ct, int k, const double* y, double* z, int64_t n) {
+    if (k <= 0) return;
+    Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * n * (k + 1));
+    const size_t smem = sizeof(double) * (k + kGT / 32);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        MG_CUDA(cudaFuncSetAttribute(k_gram_b, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = smem;
+    }
+    k_gram_b<<<std::min(tile_grid(c, n, 8), kRedBlocks), kGT, smem, c.s>>>(ct, k - 1, y, z, n, nullptr, nullptr,
+                                                                           nullptr, 1, nullptr);
+    check_launch("basis combine");
+}
+
+}  // namespace mg

@@ -88,6 +88,23 @@ void nrm2(Ctx& c, const double* a, int64_t n, double* out_dev);
 // hprev is read from device memory (the previous dot), so no host sync.
 void mgs_step(Ctx& c, double* w, const double* vprev, const double* hprev, const double* vcur,
               int64_t n, double* hout, bool accumulate, double* hsum, const int* gate);
+// Gram-form MGS sweep (gram.cu): with the basis v_0..v_k (device pointer table
+// vt), h = (I + L)^-1 V^T w (h += when accumulate), w -= V h; gt (ld x ld,
+// transposed Gram lower part) gains the row of v_k when want_q; pre_norm =
+// ||w|| before (when non-null), post_norm = ||w|| after.  Gated on *gate.
+// The Krylov basis is stored in chunks of kBasisChunk vectors, tile-major
+// ([tile][vector][kBasisTile rows]); tab[c] = chunk c.
+constexpr int kBasisTile = 2048;
+constexpr int kBasisChunk = 8;
+int64_t basis_chunk_doubles(int64_t n);
+void gram_set_ptr(Ctx& c, double** tab, int i, double* p);
+void basis_put(Ctx& c, double* chunk, int j, const double* x, double a, int64_t n);  // v_j = x / a
+void basis_get(Ctx& c, double* y, const double* chunk, int j, int64_t n);
+void basis_combine(Ctx& c, const double* const* ct, int k, const double* y, double* z, int64_t n);  // z = V_k y
+int gram_part_size(Ctx& c, int kmax);
+void gram_sweep(Ctx& c, const double* const* vt, int k, double* w, int64_t n, double* gt, int ld, double* pbuf,
+                double* h, bool accumulate, bool want_q, double* pre_norm, double* post_norm, double* part,
+                const int* gate);
 // gate_dev <- (||w|| < 0.7 * pre_norm) evaluated on device scalars
 void set_reorth_gate(Ctx& c, const double* wnorm, const double* prenorm, int* gate);
 // y = x / alpha (host scalar)
@@ -161,8 +178,29 @@ bool build_band_sched(Ctx& c, const CsrView& a, int dir, const int* glev, BandSc
 void gs_band_sweep(Ctx& c, const BandSched& s, int64_t nnz, int n, const double* b, const double* xold,
                    double* xnew);
 
+// Level-synchronous pipelined sweep schedule (gs_ls.cu): K groups of
+// consecutive rows, each a stream of program chunks processed by one warp.
+constexpr int kLsCH = 16384;  // program chunk bytes
+constexpr int kLsMaxNS = 8;   // chunks in the shared-memory ring (at most)
+constexpr int kLsClasses = 5; // dependency classes ND = 2, 4, 8, 16, 32
+struct LsSched {
+    bool ok = false;
+    int K = 0, W = 0, hmax = 0, dir = 0, nsteps = 0, nchunks = 0, maxdist = 0, smem = 0, nd = 0, ns = 0, cls = 0;
+    DBuf<char> prog;       // K groups' chunks, kLsCH bytes each
+    DBuf<int2> gch;        // per group: first chunk, chunk count
+    DBuf<int> imp;         // per group: rows imported from the previous group
+    DBuf<int2> gimp;       // per group: offset, count into imp
+    DBuf<long long> coff;  // per row: byte offset of its c' slot in prog | export bit
+};
+bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd, int dir, const int* glev, int K, LsSched& s);
+void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
+                 bool xold_zero, const LsSched& s);
+
 struct AmgLevel {
     int n = 0;
+    const int* glev_f = nullptr;      // global DAG levels of the sweep directions
+    const int* glev_b = nullptr;
+    LsSched ls_fwd, ls_bwd;           // level-synchronous sweep programs (gs_ls.cu)
     CsrView a;            // level operator (level 0 may be a non-owning view)
     DCsr a_own, p, r;     // p/r: interpolation into the finer level (levels >= 1)
     DBuf<signed char> cf; // C/F splitting of this level (levels < last)

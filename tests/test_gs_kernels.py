@@ -1,7 +1,8 @@
 """Every Gauss-Seidel sweep kernel against the oracle.
 
 The setup-time autotuner (amg_cycle.cu: tune_level_sweep) picks, per AMG
-level, the fastest of three dependency-scheduled sweep kernels; all three keep
+level, the fastest of the dependency-scheduled sweep kernels (warp per row,
+CTA band, band segment, cluster, level-synchronous pipeline); all of them keep
 the natural-order semantics of sym_gauss_seidel (amg.cpp:25-43).  Each is
 forced here (MPREC_GS_MODE) on a system large enough for the band kernels to
 engage, and the preconditioner apply / solve are checked against the oracle.
@@ -26,7 +27,7 @@ def cfg2():
     return gen.generate(2)
 
 
-@pytest.mark.parametrize("mode", ["warp", "cta", "seg", "cluster", ""])
+@pytest.mark.parametrize("mode", ["warp", "cta", "seg", "cluster", "ls", ""])
 @pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
 def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
     monkeypatch.setenv("MPREC_GS_MODE", mode)
