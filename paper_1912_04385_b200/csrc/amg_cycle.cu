@@ -527,7 +527,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     }
     // level-synchronous pipelined programs (gs_ls.cu): group counts by level size
     // (B200 measurements: 74 groups win on million-row levels, fewer below)
-    int ls_K = 0;
+    int ls_K = 0, ls_mode = 0;
     if (try_ls && sorted) {
         std::vector<int> cands;
         if (L.n >= (1 << 20))
@@ -538,22 +538,30 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
             cands = {74, 37};
         else
             cands = {37, 16};
-        for (int K : cands) {
-            L.ls_fwd = LsSched();
-            if (!build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, L.ls_fwd)) continue;
-            const float t = time_fwd();
-            if (t < t_best) {
-                t_best = t;
-                ls_K = K;
+        LsSched best;
+        int maxnd = 0;
+        for (int K : cands)
+            for (int mode : {1, 2}) {
+                if (mode == 2 && maxnd <= 4) continue;  // narrow level: fixed class only
+                L.ls_fwd = LsSched();
+                if (!build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, L.ls_fwd, mode)) continue;
+                maxnd = L.ls_fwd.nd;
+                const float t = time_fwd();
+                if (t < t_best) {
+                    t_best = t;
+                    ls_K = K;
+                    ls_mode = mode;
+                    best = std::move(L.ls_fwd);
+                }
             }
-        }
-        L.ls_fwd = LsSched();
+        L.ls_fwd = std::move(best);
     }
     if (ls_K > 0) {
         best_mode = 4;
-        build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, ls_K, L.ls_fwd);
-        build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, ls_K, L.ls_bwd);
+        build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, ls_K, L.ls_bwd, ls_mode);
         if (!L.ls_bwd.ok) L.ls_fwd = LsSched();  // both directions or neither
+    } else {
+        L.ls_fwd = LsSched();
     }
     if (best_mode != 2) {
         L.seg_fwd = SegSched();

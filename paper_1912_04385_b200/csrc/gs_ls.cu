@@ -296,6 +296,145 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
     }
 }
 
+// Variable-width records (levels whose widest row has more than 4
+// dependencies): the step header's class field is nd4 = ceil(widest row / 4),
+// the record of lane q is
+//   +0 int4 sl[0..3] | +16 double c' | +24 int row, myslot | +32 double e[0..3]
+//   +64 + 48 (g - 1): int4 sl[4g..4g+3], double e[4g..4g+3]    (g = 1 .. nd4 - 1)
+// padded to an odd number of 16-byte units (conflict-free lane-strided loads).
+// Only the step's own width is loaded and summed (warp-uniform group loop), so
+// a few wide rows no longer widen every record of the level.
+__host__ __device__ constexpr int ls_rsv(int nd4) {
+    return (16 + 48 * nd4) + ((((16 + 48 * nd4) >> 4) & 1) ? 0 : 16);
+}
+
+__device__ __forceinline__ double ls_quad(const volatile double* xs, int4 sl, const double* e) {
+    const double x0 = xs[sl.x], x1 = xs[sl.y], x2 = xs[sl.z], x3 = xs[sl.w];
+    const double2 a = reinterpret_cast<const double2*>(e)[0], b = reinterpret_cast<const double2*>(e)[1];
+    return fma(a.x, x0, a.y * x1) + fma(b.x, x2, b.y * x3);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_gs_lsv(const char* __restrict__ prog, const int2* __restrict__ gch,
+                                                         const int* __restrict__ imp, const int2* __restrict__ gimp,
+                                                         double* xnew, int W, int trash, int ns) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    char* ring = reinterpret_cast<char*>(sm);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ns * kLsCH);
+    uint64_t* empty = full + ns;
+    int* imported = reinterpret_cast<int*>(empty + ns);
+    double* xs = reinterpret_cast<double*>(sm + ns * kLsCH + 2 * ns * 8 + 16);
+    const int g = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int2 ch = gch[g];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ns; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        *imported = 0;
+        xs[W] = 0.0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 2) {
+        if (lane == 0)
+            for (int c = 0; c < ch.y; ++c) {
+                const int s = c & (ns - 1);
+                if (c >= ns) mbar_wait(empty + s, ((c / ns) - 1) & 1);
+                mbar_expect_tx(full + s, kLsCH);
+                bulk_g2s(ring + s * kLsCH, prog + (int64_t)(ch.x + c) * kLsCH, kLsCH, full + s);
+            }
+        return;
+    }
+    if (warp == 1) {
+        const int2 gi = gimp[g];
+        const int* rows = imp + gi.x;
+        const int nimp = gi.y;
+        volatile double* halo = xs + W + 1;
+        volatile int* vimp = imported;
+        int base = 0;
+        while (base < nimp) {
+            const int idx = base + lane;
+            const bool in = idx < nimp;
+            unsigned long long raw = kPending;
+            if (in) raw = ld_relaxed_ls(xnew + __ldg(rows + idx));
+            const bool ready = in && raw != kPending;
+            const unsigned m = __ballot_sync(0xffffffffu, ready);
+            const int pre = min(m == 0xffffffffu ? 32 : __ffs(~m) - 1, nimp - base);
+            if (lane < pre) halo[idx] = __longlong_as_double((long long)raw);
+            if (pre > 0) {
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    *vimp = base + pre;
+                }
+                base += pre;
+            }
+        }
+        return;
+    }
+    const volatile double* vxs = xs;
+    const unsigned imp_a = smem_u32(imported);
+    int have = 0;
+    for (int c = 0; c < ch.y; ++c) {
+        const int slot = c & (ns - 1);
+        mbar_wait(full + slot, (c / ns) & 1);
+        const char* st = ring + slot * kLsCH;
+        const int nsteps = *reinterpret_cast<const int*>(st);
+        st += 16;
+        int4 h = *reinterpret_cast<const int4*>(st);
+        int4 s0 = *reinterpret_cast<const int4*>(st + 16 + min(lane, h.x - 1) * ls_rsv(h.y));
+        for (int k = 0; k < nsteps; ++k) {
+            asm volatile(
+                "{\n .reg .pred p;\n .reg .s32 r;\n"
+                " setp.le.s32 p, %2, %0;\n"
+                " @p bra.uni LSD%=;\n"
+                "LSW%=:\n ld.volatile.shared.s32 r, [%1];\n setp.lt.s32 p, r, %2;\n @p bra.uni LSW%=;\n"
+                " mov.s32 %0, r;\n fence.acq_rel.cta;\n"
+                "LSD%=:\n}"
+                : "+r"(have)
+                : "r"(imp_a), "r"(h.z)
+                : "memory");
+            const char* rec = st + 16 + min(lane, h.x - 1) * ls_rsv(h.y);
+            const double x0 = vxs[s0.x], x1 = vxs[s0.y], x2 = vxs[s0.z], x3 = vxs[s0.w];
+            // next step: header, then its first slot group
+            const char* stn = st + h.w;
+            int4 hn;
+            asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(hn.x), "=r"(hn.y), "=r"(hn.z), "=r"(hn.w)
+                         : "r"(smem_u32(stn)));
+            const bool more = k + 1 < nsteps;
+            const int4 s0n = *reinterpret_cast<const int4*>((more ? stn : st) + 16 +
+                                                           min(lane, (more ? hn.x : h.x) - 1) *
+                                                               ls_rsv(more ? hn.y : h.y));
+            const double cc = *reinterpret_cast<const double*>(rec + 16);
+            const int2 rs = *reinterpret_cast<const int2*>(rec + 24);
+            const double2 ea = reinterpret_cast<const double2*>(rec + 32)[0], eb = reinterpret_cast<const double2*>(rec + 32)[1];
+            double acc = fma(ea.x, x0, ea.y * x1) + fma(eb.x, x2, eb.y * x3);
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                if (q < h.y) {
+                    const char* gq = rec + 64 + 48 * (q - 1);
+                    acc += ls_quad(vxs, *reinterpret_cast<const int4*>(gq), reinterpret_cast<const double*>(gq + 16));
+                }
+            const double x = cc - acc;
+            const int row = lane < h.x ? rs.x : -1;
+            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(xs + (lane < h.x ? rs.y : trash))), "d"(x)
+                         : "memory");
+            asm volatile(
+                "{\n .reg .pred p;\n setp.ge.s32 p, %2, 0;\n @p st.relaxed.gpu.global.b64 [%0], %1;\n}" ::"l"(xnew + row),
+                "l"(__double_as_longlong(x)), "r"(row)
+                : "memory");
+            __syncwarp();
+            st = stn;
+            h = hn;
+            s0 = s0n;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
+    }
+}
+
 __global__ void k_ls_testvec(double* b, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) b[i] = 1.5 + sin(0.37 * i);
@@ -310,7 +449,7 @@ int ls_smem_bytes(int W, int hmax, int ns) { return ns * kLsCH + 2 * ns * 8 + 16
 // s.ok = false) when the level does not fit the scheme: a dependency reaching
 // beyond the previous group, or a ring + halo larger than shared memory.
 bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, const int* glev_dev, int K,
-                    LsSched& s) {
+                    LsSched& s, int rec_mode) {
     s = LsSched();
     const int n = a.n;
     if (n < 64 || K < 1) return false;
@@ -344,7 +483,7 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
     std::vector<int> nd(n);
     int maxnd = 0;
     for (int i = 0; i < n; ++i) maxnd = std::max(maxnd, nd[i] = ndeps(i));
-    if (maxnd > ls_nd(kLsClasses - 1)) return false;
+    if (maxnd > 32) return false;
     // processing order inside each group: (level, dependency count, sweep index) --
     // sorting a level's rows by width keeps wide rows together in few steps
     std::vector<int> seq(n), pos(n);
@@ -393,6 +532,9 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
     // programs: one dependency class for the whole level (kernel template)
     int cls = 0;
     while (ls_nd(cls) < maxnd) ++cls;
+    // variable-width records (k_gs_lsv) for wide levels unless fixed-class forced
+    const bool var = rec_mode == 2 || (rec_mode == 0 && maxnd > 4);
+    if (var) cls = kLsVar;
     std::vector<char> prog;
     std::vector<int2> gch(K);
     std::vector<long long> coff(n);
@@ -405,9 +547,19 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
         int off = kLsCH;
         for (int u = 0; u < m;) {
             const int L = lev[q[u]];
-            int cnt = 0;
-            while (u + cnt < m && cnt < 32 && lev[q[u + cnt]] == L && 16 + (cnt + 1) * ls_rs(cls) <= kLsCH - 16) ++cnt;
-            const int RS = ls_rs(cls), ND = ls_nd(cls), bytes = 16 + cnt * RS;
+            int cnt = 0, nd4 = 1;
+            if (var) {
+                while (u + cnt < m && cnt < 32 && lev[q[u + cnt]] == L) {
+                    const int n4 = std::max(nd4, (nd[q[u + cnt]] + 3) / 4);
+                    if (16 + (cnt + 1) * ls_rsv(n4) > kLsCH - 16) break;
+                    nd4 = n4;
+                    ++cnt;
+                }
+            } else {
+                while (u + cnt < m && cnt < 32 && lev[q[u + cnt]] == L && 16 + (cnt + 1) * ls_rs(cls) <= kLsCH - 16)
+                    ++cnt;
+            }
+            const int RS = var ? ls_rsv(nd4) : ls_rs(cls), ND = var ? 4 * nd4 : ls_nd(cls), bytes = 16 + cnt * RS;
             if (off + bytes > kLsCH) {
                 cbase = nchunks * int64_t(kLsCH);
                 prog.resize(size_t(cbase + kLsCH), 0);
@@ -422,22 +574,30 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
                 int* sl0 = reinterpret_cast<int*>(rec);
                 double* cp = reinterpret_cast<double*>(rec + 16);
                 int* rsl = reinterpret_cast<int*>(rec + 24);
-                double* ep = reinterpret_cast<double*>(rec + 32);
+                double* ep0 = reinterpret_cast<double*>(rec + 32);
                 int* sl1 = reinterpret_cast<int*>(rec + 32 + 8 * ND);
-                auto slot = [&](int d) -> int& { return d < 4 ? sl0[d] : sl1[d - 4]; };
+                auto slot = [&](int d) -> int& {
+                    if (d < 4) return sl0[d];
+                    if (var) return reinterpret_cast<int*>(rec + 64 + 48 * (d / 4 - 1))[d % 4];
+                    return sl1[d - 4];
+                };
+                auto coef = [&](int d) -> double& {
+                    if (var && d >= 4) return reinterpret_cast<double*>(rec + 64 + 48 * (d / 4 - 1) + 16)[d % 4];
+                    return ep0[d];
+                };
                 *cp = 0.0;
                 rsl[0] = i;
                 rsl[1] = pos[i] & (W - 1);
                 coff[i] = (cbase + off + 16 + r * RS + 16) | (exported[i] ? 1 : 0);
                 for (int d = 0; d < std::max(ND, 4); ++d) {
-                    if (d < ND) ep[d] = 0.0;
+                    if (d < ND) coef(d) = 0.0;
                     if (d < 4 || d < ND) slot(d) = W;
                 }
                 int d = 0;
                 for (int k = rp[i]; k < rp[i + 1]; ++k) {
                     const int j = ci[k];
                     if (!is_dep(i, j)) continue;
-                    ep[d] = v[k] * invd[i];
+                    coef(d) = v[k] * invd[i];
                     if (gid[j] == g) {
                         slot(d) = pos[j] & (W - 1);
                     } else {
@@ -447,7 +607,7 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
                     ++d;
                 }
             }
-            const int hdr[4] = {cnt, cls, need, bytes};
+            const int hdr[4] = {cnt, var ? nd4 : cls, need, bytes};
             std::memcpy(base, hdr, 16);
             *reinterpret_cast<int*>(prog.data() + cbase) += 1;
             off += bytes;
@@ -502,6 +662,16 @@ void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, 
                                                     s.dir, s.coff.p, s.prog.p, xnew);
         check_launch("gs ls pre");
         switch (s.cls) {
+            case kLsVar: {
+                static bool attr = false;
+                if (!attr) {
+                    MG_CUDA(cudaFuncSetAttribute(k_gs_lsv, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+                    attr = true;
+                }
+                k_gs_lsv<<<s.K, kThreads, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, xnew, s.W,
+                                                         s.W + 1 + s.hmax, s.ns);
+                break;
+            }
             case 0: launch_ls<2>(c, s, xnew); break;
             case 1: launch_ls<4>(c, s, xnew); break;
             case 2: launch_ls<8>(c, s, xnew); break;
@@ -522,8 +692,9 @@ void gs_ls_experiment(Ctx& c, Amg& amg, int l, int K, int reps, double* out) {
     AmgLevel& L = *amg.lv[l];
     for (int q = 0; q < 10; ++q) out[q] = 0.0;
     LsSched sf, sb;
-    const bool okf = build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, sf);
-    const bool okb = okf && build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, K, sb);
+    const int rm = getenv("MPREC_LS_REC") ? atoi(getenv("MPREC_LS_REC")) : 0;
+    const bool okf = build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, sf, rm);
+    const bool okb = okf && build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, K, sb, rm);
     out[9] = (okf && okb) ? 1.0 : 0.0;
     if (!okf || !okb) return;
     out[6] = sf.W;

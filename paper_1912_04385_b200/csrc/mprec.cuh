@@ -183,6 +183,7 @@ void gs_band_sweep(Ctx& c, const BandSched& s, int64_t nnz, int n, const double*
 constexpr int kLsCH = 16384;  // program chunk bytes
 constexpr int kLsMaxNS = 8;   // chunks in the shared-memory ring (at most)
 constexpr int kLsClasses = 5; // dependency classes ND = 2, 4, 8, 16, 32
+constexpr int kLsVar = 9;     // class id of variable-width records (k_gs_lsv)
 struct LsSched {
     bool ok = false;
     int K = 0, W = 0, hmax = 0, dir = 0, nsteps = 0, nchunks = 0, maxdist = 0, smem = 0, nd = 0, ns = 0, cls = 0;
@@ -191,8 +192,12 @@ struct LsSched {
     DBuf<int> imp;         // per group: rows imported from the previous group
     DBuf<int2> gimp;       // per group: offset, count into imp
     DBuf<long long> coff;  // per row: byte offset of its c' slot in prog | export bit
+    int rec_mode = 0;      // how it was built (build_ls_sched)
 };
-bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd, int dir, const int* glev, int K, LsSched& s);
+// rec_mode: 0 auto (variable-width records when a row has > 4 dependencies),
+// 1 fixed class (k_gs_ls<ND>), 2 variable width (k_gs_lsv)
+bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd, int dir, const int* glev, int K, LsSched& s,
+                    int rec_mode = 0);
 void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
                  bool xold_zero, const LsSched& s);
 
