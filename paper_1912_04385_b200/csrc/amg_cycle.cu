@@ -317,10 +317,11 @@ void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
     }
     AmgLevel& N = *lv[l + 1];
     const int64_t n = L.n;
-    // x = 0; sym GS
-    fill_pending(c, L.xf.p, n);
+    // x = 0; sym GS (the level-synchronous programs mark their own exported rows)
+    const bool pend = !L.ls_fwd.ok;
+    if (pend) fill_pending(c, L.xf.p, n);
     level_sweep(c, L, r, nullptr, L.xf.p, +1, true);
-    fill_pending(c, x, n);
+    if (pend) fill_pending(c, x, n);
     level_sweep(c, L, r, L.xf.p, x, -1, false);
     // rc = R (r - A x)
     csr_spmv(c, L.a, x, L.t.p, r, false, MPREC_K_CSR);
@@ -329,9 +330,9 @@ void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
     // x += P ec
     csr_spmv(c, N.p.view(), N.x.p, x, nullptr, true, MPREC_K_CSR);
     // post sym GS
-    fill_pending(c, L.xf.p, n);
+    if (pend) fill_pending(c, L.xf.p, n);
     level_sweep(c, L, r, x, L.xf.p, +1, false);
-    fill_pending(c, x, n);
+    if (pend) fill_pending(c, x, n);
     level_sweep(c, L, r, L.xf.p, x, -1, false);
 }
 
@@ -413,9 +414,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
             const char* e = getenv("MPREC_GS_LS_K");
             return e ? atoi(e) : 16;
         }();
-        if (build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, L.ls_fwd))
-            build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, K, L.ls_bwd);
-        if (!L.ls_bwd.ok) L.ls_fwd = LsSched();
+        build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd);
         return;
     }
     // candidates by size (B200 measurements): the band kernels only
@@ -435,6 +434,9 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         return;
     }
     const bool try_ls = L.glev_f && L.glev_b && L.n >= 2048;
+    // million-row levels: the level-synchronous program beats the band kernels by
+    // 3-4x, so their schedules are not built and timed
+    const bool skip_band = force.empty() && try_ls && L.n >= 50000;
     if (force.empty() && !try_cta && !try_seg && !try_cl && !try_ls) return;
     const bool sorted = csr_sorted(c, L.a);
     if (force == "seg") {
@@ -470,7 +472,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     const char* names[5] = {"row-per-warp", "cta-band", "band-segment", "cluster", "level-sync"};
     int best_mode = 0, b_best = 0;
     float t_best = force.empty() ? time_fwd() : 1e30f;
-    if ((force.empty() && try_cta) || force == "cta") {
+    if ((force.empty() && try_cta && !skip_band) || force == "cta") {
         for (int bsz : {4096, 8192}) {
             if (L.n < 2 * bsz) continue;
             L.cta_B = bsz;
@@ -485,7 +487,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         L.cta_B = 0;
     }
     int seg_best = 0;
-    if (sorted && ((force.empty() && try_seg) || force == "seg")) {
+    if (sorted && ((force.empty() && try_seg && !skip_band) || force == "seg")) {
         build_seg_sched(c, L.a, L.seg_fwd, L.seg_bwd);
         L.seg = true;
         for (int bsz : {4096, 8192}) {
@@ -527,42 +529,36 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     }
     // level-synchronous pipelined programs (gs_ls.cu): group counts by level size
     // (B200 measurements: 74 groups win on million-row levels, fewer below)
-    int ls_K = 0, ls_mode = 0;
+    int ls_K = 0;
     if (try_ls && sorted) {
+        // group counts by level size (B200 measurements); both
+        // directions are built together, the forward program is timed
         std::vector<int> cands;
         if (L.n >= (1 << 20))
             cands = {74};
         else if (L.n >= 300000)
-            cands = {148, 74};
+            cands = {148};
         else if (L.n >= 50000)
-            cands = {74, 37};
+            cands = {74};
         else
             cands = {37, 16};
-        LsSched best;
-        int maxnd = 0;
-        for (int K : cands)
-            for (int mode : {1, 2}) {
-                if (mode == 2 && maxnd <= 4) continue;  // narrow level: fixed class only
-                L.ls_fwd = LsSched();
-                if (!build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, L.ls_fwd, mode)) continue;
-                maxnd = L.ls_fwd.nd;
-                const float t = time_fwd();
-                if (t < t_best) {
-                    t_best = t;
-                    ls_K = K;
-                    ls_mode = mode;
-                    best = std::move(L.ls_fwd);
-                }
+        LsSched bf, bb;
+        for (int K : cands) {
+            if (!build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) continue;
+            LsSched keep_b = std::move(L.ls_bwd);
+            L.ls_bwd = LsSched();
+            const float t = time_fwd();
+            if (t < t_best) {
+                t_best = t;
+                ls_K = K;
+                bf = std::move(L.ls_fwd);
+                bb = std::move(keep_b);
             }
-        L.ls_fwd = std::move(best);
+        }
+        L.ls_fwd = std::move(bf);
+        L.ls_bwd = std::move(bb);
     }
-    if (ls_K > 0) {
-        best_mode = 4;
-        build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, ls_K, L.ls_bwd, ls_mode);
-        if (!L.ls_bwd.ok) L.ls_fwd = LsSched();  // both directions or neither
-    } else {
-        L.ls_fwd = LsSched();
-    }
+    if (ls_K > 0) best_mode = 4;
     if (best_mode != 2) {
         L.seg_fwd = SegSched();
         L.seg_bwd = SegSched();

@@ -36,6 +36,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 #include "mprec.cuh"
@@ -448,22 +449,23 @@ int ls_smem_bytes(int W, int hmax, int ns) { return ns * kLsCH + 2 * ns * 8 + 16
 // Build the group programs of one sweep direction.  Returns false (and leaves
 // s.ok = false) when the level does not fit the scheme: a dependency reaching
 // beyond the previous group, or a ring + halo larger than shared memory.
-bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, const int* glev_dev, int K,
-                    LsSched& s, int rec_mode) {
-    s = LsSched();
-    const int n = a.n;
-    if (n < 64 || K < 1) return false;
+// Host-side program of one sweep direction (built from a host copy of the level).
+struct LsBuilt {
+    bool ok = false;
+    int K = 0, W = 0, hmax = 0, dir = 0, nsteps = 0, nchunks = 0, maxdist = 0, nd = 0, ns = 0, cls = 0;
+    std::vector<char> prog;
+    std::vector<int2> gch, gimp;
+    std::vector<int> imp;
+    std::vector<long long> coff;
+};
+
+static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci, const std::vector<double>& v,
+                          const std::vector<int>& lev, const std::vector<double>& invd, int n, int dir, int K,
+                          int rec_mode, LsBuilt& out) {
+    out = LsBuilt();
+    if (n < 64 || K < 1) return;
     K = std::min(K, n / 32);
-    if (K < 1) return false;
-    std::vector<int> rp(n + 1), ci(a.nnz), diag(n), lev(n);
-    std::vector<double> v(a.nnz), invd(n);
-    MG_CUDA(cudaMemcpyAsync(rp.data(), a.rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, c.s));
-    MG_CUDA(cudaMemcpyAsync(ci.data(), a.ci, sizeof(int) * a.nnz, cudaMemcpyDeviceToHost, c.s));
-    MG_CUDA(cudaMemcpyAsync(v.data(), a.v, sizeof(double) * a.nnz, cudaMemcpyDeviceToHost, c.s));
-    MG_CUDA(cudaMemcpyAsync(diag.data(), a.diag, sizeof(int) * n, cudaMemcpyDeviceToHost, c.s));
-    MG_CUDA(cudaMemcpyAsync(lev.data(), glev_dev, sizeof(int) * n, cudaMemcpyDeviceToHost, c.s));
-    MG_CUDA(cudaMemcpyAsync(invd.data(), invd_dev, sizeof(double) * n, cudaMemcpyDeviceToHost, c.s));
-    c.sync();
+    if (K < 1) return;
     auto row_of_t = [&](int t) { return dir > 0 ? t : n - 1 - t; };
     auto is_dep = [&](int i, int j) { return dir > 0 ? j < i : j > i; };
     std::vector<int> gstart(K + 1), gid(n);
@@ -473,7 +475,7 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
     for (int i = 0; i < n; ++i)
         for (int k = rp[i]; k < rp[i + 1]; ++k) {
             const int j = ci[k];
-            if (is_dep(i, j) && gid[j] != gid[i] && gid[j] != gid[i] - 1) return false;
+            if (is_dep(i, j) && gid[j] != gid[i] && gid[j] != gid[i] - 1) return;
         }
     auto ndeps = [&](int i) {
         int d = 0;
@@ -483,7 +485,7 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
     std::vector<int> nd(n);
     int maxnd = 0;
     for (int i = 0; i < n; ++i) maxnd = std::max(maxnd, nd[i] = ndeps(i));
-    if (maxnd > 32) return false;
+    if (maxnd > 32) return;
     // processing order inside each group: (level, dependency count, sweep index) --
     // sorting a level's rows by width keeps wide rows together in few steps
     std::vector<int> seq(n), pos(n);
@@ -528,12 +530,12 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
             ns = t;
             break;
         }
-    if (ns == 0) return false;
+    if (ns == 0) return;
     // programs: one dependency class for the whole level (kernel template)
     int cls = 0;
     while (ls_nd(cls) < maxnd) ++cls;
     // variable-width records (k_gs_lsv) for wide levels unless fixed-class forced
-    const bool var = rec_mode == 2 || (rec_mode == 0 && maxnd > 4);
+    const bool var = rec_mode == 2 || (rec_mode == 0 && maxnd > 16);
     if (var) cls = kLsVar;
     std::vector<char> prog;
     std::vector<int2> gch(K);
@@ -618,25 +620,106 @@ bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, c
     }
     std::vector<int2> gimp(K);
     for (int g = 0; g < K; ++g) gimp[g] = make_int2(gimp_off[g], gimp_off[g + 1] - gimp_off[g]);
-    s.prog.upload(prog.data(), prog.size(), c.s);
-    s.gch.upload(gch.data(), K, c.s);
-    s.imp.alloc(std::max<size_t>(imp.size(), 1));
-    if (!imp.empty()) s.imp.upload(imp.data(), imp.size(), c.s);
-    s.gimp.upload(gimp.data(), K, c.s);
-    s.coff.upload(coff.data(), n, c.s);
+    out.prog = std::move(prog);
+    out.gch = std::move(gch);
+    out.gimp = std::move(gimp);
+    out.imp = std::move(imp);
+    out.coff = std::move(coff);
+    out.K = K;
+    out.W = W;
+    out.hmax = hmax;
+    out.dir = dir;
+    out.nsteps = int(nsteps_total);
+    out.nchunks = int(nchunks);
+    out.maxdist = maxdist;
+    out.nd = maxnd;
+    out.ns = ns;
+    out.cls = cls;
+    out.ok = true;
+}
+
+static void ls_upload(Ctx& c, LsBuilt& b, LsSched& s) {
+    s = LsSched();
+    if (!b.ok) return;
+    s.prog.upload(b.prog.data(), b.prog.size(), c.s);
+    s.gch.upload(b.gch.data(), b.K, c.s);
+    s.imp.alloc(std::max<size_t>(b.imp.size(), 1));
+    if (!b.imp.empty()) s.imp.upload(b.imp.data(), b.imp.size(), c.s);
+    s.gimp.upload(b.gimp.data(), b.K, c.s);
+    s.coff.upload(b.coff.data(), b.coff.size(), c.s);
     c.sync();
-    s.K = K;
-    s.W = W;
-    s.hmax = hmax;
-    s.dir = dir;
-    s.nsteps = int(nsteps_total);
-    s.nchunks = int(nchunks);
-    s.maxdist = maxdist;
-    s.nd = maxnd;
-    s.ns = ns;
-    s.cls = cls;
-    s.smem = ls_smem_bytes(W, hmax, ns);
+    s.K = b.K;
+    s.W = b.W;
+    s.hmax = b.hmax;
+    s.dir = b.dir;
+    s.nsteps = b.nsteps;
+    s.nchunks = b.nchunks;
+    s.maxdist = b.maxdist;
+    s.nd = b.nd;
+    s.ns = b.ns;
+    s.cls = b.cls;
+    s.smem = ls_smem_bytes(b.W, b.hmax, b.ns);
     s.ok = true;
+}
+
+// Host copy of a level: one download serves both sweep directions.
+struct LsHost {
+    int n = 0;
+    std::vector<int> rp, ci, levf, levb;
+    std::vector<double> v, invd;
+};
+static void ls_download(Ctx& c, const CsrView& a, const double* invd_dev, const int* glev_f, const int* glev_b,
+                        LsHost& h) {
+    const int n = a.n;
+    h.n = n;
+    h.rp.resize(n + 1);
+    h.ci.resize(a.nnz);
+    h.v.resize(a.nnz);
+    h.invd.resize(n);
+    MG_CUDA(cudaMemcpyAsync(h.rp.data(), a.rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, c.s));
+    MG_CUDA(cudaMemcpyAsync(h.ci.data(), a.ci, sizeof(int) * a.nnz, cudaMemcpyDeviceToHost, c.s));
+    MG_CUDA(cudaMemcpyAsync(h.v.data(), a.v, sizeof(double) * a.nnz, cudaMemcpyDeviceToHost, c.s));
+    MG_CUDA(cudaMemcpyAsync(h.invd.data(), invd_dev, sizeof(double) * n, cudaMemcpyDeviceToHost, c.s));
+    if (glev_f) {
+        h.levf.resize(n);
+        MG_CUDA(cudaMemcpyAsync(h.levf.data(), glev_f, sizeof(int) * n, cudaMemcpyDeviceToHost, c.s));
+    }
+    if (glev_b) {
+        h.levb.resize(n);
+        MG_CUDA(cudaMemcpyAsync(h.levb.data(), glev_b, sizeof(int) * n, cudaMemcpyDeviceToHost, c.s));
+    }
+    c.sync();
+}
+
+bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, const int* glev_dev, int K,
+                    LsSched& s, int rec_mode) {
+    s = LsSched();
+    if (a.n < 64) return false;
+    LsHost h;
+    ls_download(c, a, invd_dev, dir > 0 ? glev_dev : nullptr, dir > 0 ? nullptr : glev_dev, h);
+    LsBuilt b;
+    ls_build_host(h.rp, h.ci, h.v, dir > 0 ? h.levf : h.levb, h.invd, h.n, dir, K, rec_mode, b);
+    ls_upload(c, b, s);
+    s.rec_mode = rec_mode;
+    return s.ok;
+}
+
+// Both directions from one download, the two host builds on two threads.
+bool build_ls_pair(Ctx& c, const CsrView& a, const double* invd_dev, const int* glev_f, const int* glev_b, int K,
+                   int rec_mode, LsSched& f, LsSched& bw) {
+    f = LsSched();
+    bw = LsSched();
+    if (a.n < 64) return false;
+    LsHost h;
+    ls_download(c, a, invd_dev, glev_f, glev_b, h);
+    LsBuilt bf, bb;
+    std::thread t([&] { ls_build_host(h.rp, h.ci, h.v, h.levb, h.invd, h.n, -1, K, rec_mode, bb); });
+    ls_build_host(h.rp, h.ci, h.v, h.levf, h.invd, h.n, +1, K, rec_mode, bf);
+    t.join();
+    if (!bf.ok || !bb.ok) return false;
+    ls_upload(c, bf, f);
+    ls_upload(c, bb, bw);
+    f.rec_mode = bw.rec_mode = rec_mode;
     return true;
 }
 

@@ -194,10 +194,13 @@ struct LsSched {
     DBuf<long long> coff;  // per row: byte offset of its c' slot in prog | export bit
     int rec_mode = 0;      // how it was built (build_ls_sched)
 };
-// rec_mode: 0 auto (variable-width records when a row has > 4 dependencies),
+// rec_mode: 0 auto (variable-width records when a row has > 16 dependencies),
 // 1 fixed class (k_gs_ls<ND>), 2 variable width (k_gs_lsv)
 bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd, int dir, const int* glev, int K, LsSched& s,
                     int rec_mode = 0);
+// both directions (one download of the level, two host threads)
+bool build_ls_pair(Ctx& c, const CsrView& a, const double* invd, const int* glev_f, const int* glev_b, int K,
+                   int rec_mode, LsSched& fwd, LsSched& bwd);
 void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
                  bool xold_zero, const LsSched& s);
 
