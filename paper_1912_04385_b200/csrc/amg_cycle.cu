@@ -414,7 +414,11 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
             const char* e = getenv("MPREC_GS_LS_K");
             return e ? atoi(e) : 16;
         }();
-        build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd);
+        const int rec = [] {
+            const char* e = getenv("MPREC_GS_LS_REC");  // 0 auto, 1 fixed class, 2 variable width
+            return e ? atoi(e) : 0;
+        }();
+        build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, rec, L.ls_fwd, L.ls_bwd);
         return;
     }
     // candidates by size (B200 measurements): the band kernels only

@@ -9,6 +9,9 @@
 // polls the producer's VALUES directly (ld.relaxed.gpu) -- one L2 round trip
 // per dependency hop, no separate flag word.  Block values are loaded before
 // the wait so that HBM latency overlaps the dependency chain.
+#include <algorithm>
+#include <cstdlib>
+
 #include "mprec.cuh"
 
 namespace mg {
@@ -222,6 +225,15 @@ void Ilu::factor(Ctx& c) {
         dinv.ensure((size_t)lu.nc * 64);
         k_ilu_dinv8<<<(lu.nc + 127) / 128, 128, 0, c.s>>>(lu.dpos, lu.val, lu.nc, dinv.p);
         check_launch("ilu dinv");
+        // level-synchronous solve programs (ilu_ls.cu), opt-in: MPREC_ILU_LS=<groups>.
+        // Measured slower than the warp-per-block-row kernel at c5 (28 vs 5.7 ms per
+        // sweep: each step needs 6.4 KB of factor blocks and the prefetch ring that
+        // fits next to the 128 KB halo does not cover the HBM latency), DESIGN.md §5.1
+        const int ls_k = [] {  // read per factorisation (tests toggle it)
+            const char* e = getenv("MPREC_ILU_LS");
+            return e ? atoi(e) : 0;
+        }();
+        if (ls_k > 0 && pat && !ls_fwd.ok) build_ilu_ls(c, *pat, std::min(ls_k, c.sm_count), ls_fwd, ls_bwd);
     }
 }
 
@@ -241,6 +253,17 @@ void Ilu::apply(Ctx& c, const double* r, double* y) {
     const double lower_blocks = double(lu.nnzb - lu.nc) / 2 + lu.nc;
     const double bytes = lower_blocks * (8.0 * nb2 + 4.0) + 4.0 * (lu.nc + 1) + 16.0 * nn;
     if (lu.nb > 32) throw Error(MPREC_DIMENSION, "nb > 32 not supported by the ILU solve");
+    if (lu.nb == 8 && ls_fwd.ok && ls_bwd.ok) {
+        {
+            Ctx::Scope sc(&c, MPREC_K_ILU_FWD, bytes);
+            ilu_ls_solve(c, ls_fwd, ls_fwd, true, lu.val, dinv.p, r, ybuf.p);
+        }
+        {
+            Ctx::Scope sc(&c, MPREC_K_ILU_BWD, bytes);
+            ilu_ls_solve(c, ls_bwd, ls_fwd, false, lu.val, dinv.p, ybuf.p, y);
+        }
+        return;
+    }
     {
         Ctx::Scope sc(&c, MPREC_K_ILU_FWD, bytes);
         if (lu.nb == 8)

@@ -142,12 +142,26 @@ void extract_field(Ctx& c, const BsrView& a, int f, double* vals);
 void extract_pt(Ctx& c, const BsrView& a, int* erp, int* eci, double* ev);
 
 // ---- ilu.cu ------------------------------------------------------------------
+// Level-synchronous block ILU(0) solve programs (ilu_ls.cu, nb = 8).
+struct IluLs {
+    bool ok = false;
+    int K = 0, W = 0, hmax = 0, nsteps = 0, smem = 0;
+    DBuf<char> prog;
+    DBuf<int2> gch, gimp;
+    DBuf<int> imp;
+    DBuf<double> zero;  // a zero block (missing dependencies)
+};
+bool build_ilu_ls(Ctx& c, Pattern& pat, int K, IluLs& fwd, IluLs& bwd);
+void ilu_ls_solve(Ctx& c, const IluLs& s, const IluLs& zero_owner, bool fwd, const double* val, const double* dinv,
+                  const double* rhs, double* y);
+
 struct Ilu {
     BsrView lu;           // values owned elsewhere (or by `own`)
     DBuf<double> own;     // factor storage when the Ilu owns it
     DBuf<double> ybuf;    // forward-sweep output
     DBuf<int> flags;      // factorisation ready flags
     DBuf<double> dinv;    // nb = 8: packed inverses of the diagonal blocks (apply path)
+    IluLs ls_fwd, ls_bwd; // nb = 8: level-synchronous solve programs (when the pattern fits)
     Pattern* pat = nullptr;
     int n = 0;
     // factor in place (values of lu are overwritten by L\U); throws ZERO_PIVOT/SETUP

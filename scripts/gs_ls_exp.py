@@ -12,6 +12,7 @@ from paper_1912_04385_b200.api import gpu  # noqa: E402
 cid = int(sys.argv[1])
 stage = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 Ks = [int(k) for k in sys.argv[3].split(",")] if len(sys.argv) > 3 else [148, 74, 32, 16, 8, 4, 2, 1]
+only = int(sys.argv[4]) if len(sys.argv) > 4 else -1  # a single level
 api = gpu()
 a, b, _ = gen.generate(cid)
 t0 = time.time()
@@ -22,6 +23,8 @@ f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
 h = s.stage_amg(stage)
 tot_cur = tot_best = 0.0
 for l in range(h.n_levels - 1):
+    if only >= 0 and l != only:
+        continue
     n, nnz, _ = h.level_info(l)
     best = None
     cur = None

@@ -27,9 +27,14 @@ def cfg2():
     return gen.generate(2)
 
 
-@pytest.mark.parametrize("mode", ["warp", "cta", "seg", "cluster", "ls", ""])
+@pytest.mark.parametrize("mode", ["warp", "cta", "seg", "cluster", "ls", "ls-fixed", "ls-var", ""])
 @pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
 def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
+    if mode.startswith("ls-"):
+        # level-synchronous programs with fixed-class (k_gs_ls<ND>) or variable-width
+        # (k_gs_lsv) records on every level
+        monkeypatch.setenv("MPREC_GS_LS_REC", "1" if mode == "ls-fixed" else "2")
+        mode = "ls"
     monkeypatch.setenv("MPREC_GS_MODE", mode)
     a, b, _ = cfg2
     sg = gpu.system(a).setup(method, b)
@@ -41,4 +46,18 @@ def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
     rg, ro = sg.solve(), so.solve()
     assert abs(rg.iterations - ro.iterations) <= 1
     assert rg.converged == ro.converged
+    assert rel(rg.x, ro.x) < 1e-6
+
+
+@pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
+def test_ilu_level_sync_solve(gpu, orc, cfg2, method, monkeypatch):
+    """Opt-in level-synchronous block ILU(0) solve (ilu_ls.cu) against the oracle."""
+    monkeypatch.setenv("MPREC_ILU_LS", "32")
+    a, b, _ = cfg2
+    sg = gpu.system(a).setup(method, b)
+    so = orc.system(a).setup(method, b)
+    r = random_vec(a.dim, 5)
+    assert rel(sg.apply(r), so.apply(r)) < 1e-10
+    rg, ro = sg.solve(), so.solve()
+    assert abs(rg.iterations - ro.iterations) <= 1
     assert rel(rg.x, ro.x) < 1e-6
