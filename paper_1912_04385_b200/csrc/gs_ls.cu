@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
     const volatile double* vxs = xs;
     const unsigned imp_a = smem_u32(imported);
     int have = 0;
-    long long t_start = 0, t_wait = 0, n_wait = 0;
+    long long t_start = 0;
     if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     for (int c = 0; c < ch.y; ++c) {
         const int slot = c & (ns - 1);
@@ -231,16 +231,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
         int sl[ND];
         ls_slots<ND>(st + 16 + min(lane, h.x - 1) * RS, sl);
         for (int k = 0; k < nsteps; ++k) {
-            if (stats && h.z > have) {
-                long long a, b;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a));
-                while ((have = *reinterpret_cast<volatile int*>(imported)) < h.z) {
-                }
-                __threadfence_block();
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(b));
-                t_wait += b - a;
-                ++n_wait;
-            }
             asm volatile(
                 "{\n .reg .pred p;\n .reg .s32 r;\n"
                 " setp.le.s32 p, %2, %0;\n"
@@ -252,15 +242,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
                 : "r"(imp_a), "r"(h.z)
                 : "memory");
             const char* rec = st + 16 + min(lane, h.x - 1) * RS;
-            double xv[ND];
-#pragma unroll
-            for (int d = 0; d < ND; ++d) xv[d] = vxs[sl[d]];
-            // next step: header, then its slots (garbage after the chunk's last step)
+            // next step's header first: its slots can then be loaded while this
+            // step's dependencies are summed (garbage after the chunk's last step)
             const char* stn = st + h.w;
             int4 hn;
             asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(hn.x), "=r"(hn.y), "=r"(hn.z), "=r"(hn.w)
                          : "r"(smem_u32(stn)));
+            double xv[ND];
+#pragma unroll
+            for (int d = 0; d < ND; ++d) xv[d] = vxs[sl[d]];
             const bool more = k + 1 < nsteps;  // (select, not a branch)
             ls_slots<ND>((more ? stn : st) + 16 + min(lane, (more ? hn.x : h.x) - 1) * RS, sl);
             const double cc = *reinterpret_cast<const double*>(rec + 16);
@@ -292,8 +283,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         stats[4 * g + 0] = t_start;
         stats[4 * g + 1] = t_end;
-        stats[4 * g + 2] = t_wait;
-        stats[4 * g + 3] = n_wait;
+        stats[4 * g + 2] = 0;
+        stats[4 * g + 3] = 0;
     }
 }
 
@@ -397,13 +388,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_lsv(const char* __restrict__
                 : "r"(imp_a), "r"(h.z)
                 : "memory");
             const char* rec = st + 16 + min(lane, h.x - 1) * ls_rsv(h.y);
-            const double x0 = vxs[s0.x], x1 = vxs[s0.y], x2 = vxs[s0.z], x3 = vxs[s0.w];
-            // next step: header, then its first slot group
+            // next step: header first, then (below) its first slot group
             const char* stn = st + h.w;
             int4 hn;
             asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(hn.x), "=r"(hn.y), "=r"(hn.z), "=r"(hn.w)
                          : "r"(smem_u32(stn)));
+            const double x0 = vxs[s0.x], x1 = vxs[s0.y], x2 = vxs[s0.z], x3 = vxs[s0.w];
             const bool more = k + 1 < nsteps;
             const int4 s0n = *reinterpret_cast<const int4*>((more ? stn : st) + 16 +
                                                            min(lane, (more ? hn.x : h.x) - 1) *
