@@ -306,6 +306,35 @@ __device__ __forceinline__ double ls_quad(const volatile double* xs, int4 sl, co
     return fma(a.x, x0, a.y * x1) + fma(b.x, x2, b.y * x3);
 }
 
+// dependency groups 1 .. NQ-1 of a variable-width record (NQ = the step's nd4)
+template <int NQ>
+__device__ __forceinline__ double lsv_rest(const char* rec, const volatile double* xs) {
+    constexpr int M = NQ - 1;
+    int4 sq[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) sq[q] = *reinterpret_cast<const int4*>(rec + 64 + 48 * q);
+    double xv[4 * M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+        xv[4 * q] = xs[sq[q].x];
+        xv[4 * q + 1] = xs[sq[q].y];
+        xv[4 * q + 2] = xs[sq[q].z];
+        xv[4 * q + 3] = xs[sq[q].w];
+    }
+    double p[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+        const double2 a = reinterpret_cast<const double2*>(rec + 64 + 48 * q + 16)[0];
+        const double2 b = reinterpret_cast<const double2*>(rec + 64 + 48 * q + 16)[1];
+        p[q] = fma(a.x, xv[4 * q], a.y * xv[4 * q + 1]) + fma(b.x, xv[4 * q + 2], b.y * xv[4 * q + 3]);
+    }
+#pragma unroll
+    for (int w = 1; w < M; w *= 2)
+#pragma unroll
+        for (int q = 0; q + w < M; q += 2 * w) p[q] += p[q + w];
+    return p[0];
+}
+
 __global__ void __launch_bounds__(kThreads, 1) k_gs_lsv(const char* __restrict__ prog, const int2* __restrict__ gch,
                                                          const int* __restrict__ imp, const int2* __restrict__ gimp,
                                                          double* xnew, int W, int trash, int ns) {
@@ -402,13 +431,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_lsv(const char* __restrict__
             const double cc = *reinterpret_cast<const double*>(rec + 16);
             const int2 rs = *reinterpret_cast<const int2*>(rec + 24);
             const double2 ea = reinterpret_cast<const double2*>(rec + 32)[0], eb = reinterpret_cast<const double2*>(rec + 32)[1];
-            double acc = fma(ea.x, x0, ea.y * x1) + fma(eb.x, x2, eb.y * x3);
-#pragma unroll
-            for (int q = 1; q < 8; ++q)
-                if (q < h.y) {
-                    const char* gq = rec + 64 + 48 * (q - 1);
-                    acc += ls_quad(vxs, *reinterpret_cast<const int4*>(gq), reinterpret_cast<const double*>(gq + 16));
-                }
+            // groups 1 .. nd4-1: one warp-uniform switch on the step's width, then
+            // straight-line loads (all slots, all values) and a pairwise tree
+            double rest;
+            switch (h.y) {
+                case 1: rest = 0.0; break;
+                case 2: rest = lsv_rest<2>(rec, vxs); break;
+                case 3: rest = lsv_rest<3>(rec, vxs); break;
+                case 4: rest = lsv_rest<4>(rec, vxs); break;
+                case 5: rest = lsv_rest<5>(rec, vxs); break;
+                case 6: rest = lsv_rest<6>(rec, vxs); break;
+                case 7: rest = lsv_rest<7>(rec, vxs); break;
+                default: rest = lsv_rest<8>(rec, vxs); break;
+            }
+            const double acc = (fma(ea.x, x0, ea.y * x1) + fma(eb.x, x2, eb.y * x3)) + rest;
             const double x = cc - acc;
             const int row = lane < h.x ? rs.x : -1;
             asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(xs + (lane < h.x ? rs.y : trash))), "d"(x)
@@ -526,7 +562,7 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
     int cls = 0;
     while (ls_nd(cls) < maxnd) ++cls;
     // variable-width records (k_gs_lsv) for wide levels unless fixed-class forced
-    const bool var = rec_mode == 2 || (rec_mode == 0 && maxnd > 16);
+    const bool var = rec_mode == 2 || (rec_mode == 0 && maxnd > kLsVarMin);
     if (var) cls = kLsVar;
     std::vector<char> prog;
     std::vector<int2> gch(K);

@@ -198,6 +198,7 @@ constexpr int kLsCH = 16384;  // program chunk bytes
 constexpr int kLsMaxNS = 8;   // chunks in the shared-memory ring (at most)
 constexpr int kLsClasses = 5; // dependency classes ND = 2, 4, 8, 16, 32
 constexpr int kLsVar = 9;     // class id of variable-width records (k_gs_lsv)
+constexpr int kLsVarMin = 16; // auto mode: variable-width records when a row has more dependencies
 struct LsSched {
     bool ok = false;
     int K = 0, W = 0, hmax = 0, dir = 0, nsteps = 0, nchunks = 0, maxdist = 0, smem = 0, nd = 0, ns = 0, cls = 0;
