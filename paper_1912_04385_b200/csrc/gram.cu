@@ -47,6 +47,7 @@ __device__ __forceinline__ const double* tile_base(const double* const* ct, int 
 // Per-block partial sums of p_i = <v_i, w> (i <= k), q_j = <v_j, v_k> (j < k)
 // and <w, w>, over a fixed set of tiles (tile = blockIdx.x + t * gridDim.x):
 // part[blk * stride + {0..k | k+1..2k+1 | 2k+2}].
+template <bool WQ>
 __global__ void __launch_bounds__(kGT) k_gram_a(const double* const* __restrict__ ct, int k,
                                                  const double* __restrict__ w, int64_t n, double* __restrict__ part,
                                                  int stride, int want_q, const int* __restrict__ gate) {
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(kGT) k_gram_a(const double* const* __restrict_
         for (int q = 0; q < kRPT; ++q) {
             const int r = tid + q * kGT;
             wr[q] = r < nr ? w[r0 + r] : 0.0;
-            vr[q] = (r < nr && want_q) ? vkp[r] : 0.0;
+            vr[q] = (WQ && r < nr) ? vkp[r] : 0.0;
         }
         for (int c = 0; c <= ck; ++c) {
             const double* base = tile_base(ct, c, tile);
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(kGT) k_gram_a(const double* const* __restrict_
                         const int r = tid + q * kGT;
                         const double x = r < nr ? __ldcs(base + j * kT + r) : 0.0;
                         ap[j] += x * wr[q];
-                        aq[j] += x * vr[q];
+                        if (WQ) aq[j] += x * vr[q];
                     }
                 }
             }
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(kGT) k_gram_a(const double* const* __restrict_
 #pragma unroll
             for (int j = 0; j < kGV; ++j) {
                 ap[j] = warp_sum(ap[j]);
-                aq[j] = warp_sum(aq[j]);
+                if (WQ) aq[j] = warp_sum(aq[j]);
             }
             aw = warp_sum(aw);
             __syncthreads();  // previous chunk's red consumed
@@ -289,10 +290,14 @@ void gram_sweep(Ctx& c, const double* const* ct, int k, double* w, int64_t n, do
         const size_t smem = sizeof(double) * (stride + (kGT / 32) * kGRed);
         static size_t attr = 0;
         if (smem > 48 * 1024 && smem > attr) {
-            MG_CUDA(cudaFuncSetAttribute(k_gram_a, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            MG_CUDA(cudaFuncSetAttribute(k_gram_a<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            MG_CUDA(cudaFuncSetAttribute(k_gram_a<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             attr = smem;
         }
-        k_gram_a<<<grid_a, kGT, smem, c.s>>>(ct, k, w, n, part, stride, want_q ? 1 : 0, gate);
+        if (want_q)
+            k_gram_a<true><<<grid_a, kGT, smem, c.s>>>(ct, k, w, n, part, stride, 1, gate);
+        else
+            k_gram_a<false><<<grid_a, kGT, smem, c.s>>>(ct, k, w, n, part, stride, 0, gate);
         check_launch("gram pass A");
     }
     {
