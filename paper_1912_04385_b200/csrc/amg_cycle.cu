@@ -440,7 +440,6 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     const bool try_ls = L.glev_f && L.glev_b && L.n >= 2048;
     // million-row levels: the level-synchronous program beats the band kernels by
     // 3-4x, so their schedules are not built and timed
-    const bool skip_band = force.empty() && try_ls && L.n >= 50000;
     if (force.empty() && !try_cta && !try_seg && !try_cl && !try_ls) return;
     const bool sorted = csr_sorted(c, L.a);
     if (force == "seg") {
@@ -475,6 +474,41 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     };
     const char* names[5] = {"row-per-warp", "cta-band", "band-segment", "cluster", "level-sync"};
     int best_mode = 0, b_best = 0;
+    // level-synchronous programs (gs_ls.cu) first: on levels above 50k rows they
+    // beat the band kernels by 2-4x, so those are only built and
+    // timed when no LS program fits the level.  Group counts by level size, the
+    // next candidate tried only when a program does not fit (dependency beyond
+    // the previous group, shared memory); both directions built together.
+    int ls_K = 0;
+    LsSched ls_bf, ls_bb;
+    float t_ls = 1e30f;
+    if (try_ls && sorted && force.empty()) {
+        std::vector<int> cands;
+        if (L.n >= (1 << 20))
+            cands = {74, 148, 37};
+        else if (L.n >= 300000)
+            cands = {148, 74, 37};
+        else if (L.n >= 50000)
+            cands = {74, 148, 37};
+        else
+            cands = {37, 16, 8};
+        const bool first_fit = L.n >= 50000;  // large levels: the first program that fits
+        for (int K : cands) {
+            if (!build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) continue;
+            LsSched keep_b = std::move(L.ls_bwd);
+            L.ls_bwd = LsSched();
+            const float t = time_fwd();
+            if (t < t_ls) {
+                t_ls = t;
+                ls_K = K;
+                ls_bf = std::move(L.ls_fwd);
+                ls_bb = std::move(keep_b);
+            }
+            L.ls_fwd = LsSched();
+            if (first_fit) break;
+        }
+    }
+    const bool skip_band = ls_K > 0 && L.n >= 50000;
     float t_best = force.empty() ? time_fwd() : 1e30f;
     if ((force.empty() && try_cta && !skip_band) || force == "cta") {
         for (int bsz : {4096, 8192}) {
@@ -531,38 +565,17 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
             }
         }
     }
-    // level-synchronous pipelined programs (gs_ls.cu): group counts by level size
-    // (B200 measurements: 74 groups win on million-row levels, fewer below)
-    int ls_K = 0;
-    if (try_ls && sorted) {
-        // group counts by level size (B200 measurements); both
-        // directions are built together, the forward program is timed
-        std::vector<int> cands;
-        if (L.n >= (1 << 20))
-            cands = {74};
-        else if (L.n >= 300000)
-            cands = {148};
-        else if (L.n >= 50000)
-            cands = {74};
-        else
-            cands = {37, 16};
-        LsSched bf, bb;
-        for (int K : cands) {
-            if (!build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) continue;
-            LsSched keep_b = std::move(L.ls_bwd);
-            L.ls_bwd = LsSched();
-            const float t = time_fwd();
-            if (t < t_best) {
-                t_best = t;
-                ls_K = K;
-                bf = std::move(L.ls_fwd);
-                bb = std::move(keep_b);
-            }
-        }
-        L.ls_fwd = std::move(bf);
-        L.ls_bwd = std::move(bb);
+    // the level-synchronous program when it is the fastest candidate
+    if (ls_K > 0 && t_ls < t_best) {
+        t_best = t_ls;
+        best_mode = 4;
+        L.ls_fwd = std::move(ls_bf);
+        L.ls_bwd = std::move(ls_bb);
+    } else {
+        ls_K = 0;
+        L.ls_fwd = LsSched();
+        L.ls_bwd = LsSched();
     }
-    if (ls_K > 0) best_mode = 4;
     if (best_mode != 2) {
         L.seg_fwd = SegSched();
         L.seg_bwd = SegSched();
