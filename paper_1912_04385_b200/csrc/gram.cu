@@ -90,21 +90,43 @@ __global__ void __launch_bounds__(kGT) k_gram_a(const double* const* __restrict_
             if (c == 0)
 #pragma unroll
                 for (int q = 0; q < kRPT; ++q) aw += wr[q] * wr[q];
+            // butterfly reduction of all V partial sums at once (V - 1 + 5 - log2 V
+            // shuffles instead of 5 V): after it, lane l holds the warp total of
+            // value idx(l) when l has no bits below the last halving offset
+            constexpr int V = WQ ? 2 * kGV : kGV;
+            double vv[V];
 #pragma unroll
             for (int j = 0; j < kGV; ++j) {
-                ap[j] = warp_sum(ap[j]);
-                if (WQ) aq[j] = warp_sum(aq[j]);
+                vv[j] = ap[j];
+                if (WQ) vv[kGV + j] = aq[j];
             }
-            aw = warp_sum(aw);
-            __syncthreads();  // previous chunk's red consumed
-            if (lane == 0) {
+            int idx = 0;
 #pragma unroll
-                for (int j = 0; j < kGV; ++j) {
-                    red[wid * kGRed + j] = ap[j];
-                    red[wid * kGRed + kGV + j] = aq[j];
+            for (int cnt = V, o = 16; cnt > 1; cnt /= 2, o /= 2) {
+                const bool up = lane & o;
+#pragma unroll
+                for (int i = 0; i < cnt / 2; ++i) {
+                    const double send = up ? vv[i] : vv[i + cnt / 2];
+                    const double keep = up ? vv[i + cnt / 2] : vv[i];
+                    vv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
-                red[wid * kGRed + 2 * kGV] = aw;
+                if (up) idx += cnt / 2;
             }
+            // remaining lanes bits below the last offset: plain xor reduction
+            constexpr int LOG_V = (V == 16) ? 4 : 3;
+#pragma unroll
+            for (int o = 16 >> LOG_V; o > 0; o >>= 1) vv[0] += __shfl_xor_sync(0xffffffffu, vv[0], o);
+            if (c == 0) aw = warp_sum(aw);
+            __syncthreads();  // previous chunk's red consumed
+            if ((lane & ((32 >> LOG_V) - 1)) == 0) {
+                if (WQ)
+                    red[wid * kGRed + idx] = vv[0];
+                else {
+                    red[wid * kGRed + idx] = vv[0];
+                    red[wid * kGRed + kGV + idx] = 0.0;
+                }
+            }
+            if (lane == 0) red[wid * kGRed + 2 * kGV] = aw;
             __syncthreads();
             if (tid < kGRed) {
                 double s = 0.0;
