@@ -11,9 +11,11 @@
 //     y_I = inv(L_II) v (forward, unit lower)  /  inv(U_II) v (backward)
 // with the packed inverses of the diagonal blocks (k_ilu_dinv8).  The block
 // values are NOT copied into the program (they are the 10 GB factor): the
-// compute warp prefetches the blocks of the step P steps ahead straight from
-// the factor with cp.async (16-byte chunks, one commit group per step) into a
-// shared-memory ring, so HBM latency leaves the dependency chain.
+// compute warp prefetches the blocks of the step P = 20 steps ahead straight
+// from the factor with cp.async (16-byte chunks; completion tracked by one
+// mbarrier per ring slot via cp.async.mbarrier.arrive) into a shared-memory
+// ring, so HBM latency leaves the dependency chain.  The import halo is a ring
+// of 256 block rows; the importer is held back by the consumer's progress.
 #include <algorithm>
 #include <cstring>
 #include <thread>
@@ -28,7 +30,8 @@ constexpr int kIB = 4;                   // block rows per step
 constexpr int kIStep = 16 + kIB * 24;    // program bytes per step
 constexpr int kISPC = kLsCH / kIStep;    // steps per program chunk
 constexpr int kIChunk = kISPC * kIStep;  // program chunk bytes
-constexpr int kIP = 6;                   // prefetch distance (steps)
+constexpr int kIP = 20;                  // prefetch distance (steps)
+constexpr int kIH = 256;                 // halo ring entries (block rows)
 constexpr int kIBlk = kIB * 200;         // doubles per prefetched step: 4 x (3 blocks + rhs)
 constexpr int kINS = 2;                  // program chunks in the ring
 constexpr int kIThreads = 96;
@@ -104,8 +107,10 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
     double* blk = reinterpret_cast<double*>(sm + kINS * kLsCH);           // prefetched blocks
     uint64_t* full = reinterpret_cast<uint64_t*>(blk + kIP * kIBlk);
     uint64_t* empty = full + kINS;
-    int* imported = reinterpret_cast<int*>(empty + kINS);
-    double* xs = reinterpret_cast<double*>(imported + 4);                 // 8W ring | zero 8 | trash 8 | halo
+    uint64_t* slotbar = empty + kINS;                                     // prefetch slots (cp.async arrivals)
+    int* imported = reinterpret_cast<int*>(slotbar + kIP);
+    volatile int* cons = imported + 1;                                   // consumer's current need
+    double* xs = reinterpret_cast<double*>(imported + 4);                 // 8W ring | zero 8 | trash 8 | halo ring
     const int g = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int2 ch = gch[g];  // first chunk, steps
@@ -115,7 +120,9 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
         }
+        for (int s = 0; s < kIP; ++s) mbar_init(slotbar + s, 32);
         *imported = 0;
+        *cons = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = threadIdx.x; i < 16; i += blockDim.x) xs[8 * W + i] = 0.0;
@@ -139,6 +146,10 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
         const int e = lane >> 3, r = lane & 7;
         int base = 0;
         while (base < nimp) {
+            // ring back-pressure: entry idx overwrites idx - kIH, which is dead once
+            // the consumer's need passed idx - kIH / 2 (checked at setup)
+            while (base + 4 > *cons + kIH / 2) {
+            }
             const int idx = base + e;
             const bool in = idx < nimp;
             unsigned long long raw = kPending;
@@ -148,7 +159,7 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
             int pre = 0;
             while (pre < 4 && ((m >> (8 * pre)) & 0xffu) == 0xffu) ++pre;
             pre = min(pre, nimp - base);
-            if (e < pre) halo[int64_t(idx) * 8 + r] = __longlong_as_double((long long)raw);
+            if (e < pre) halo[int64_t(idx & (kIH - 1)) * 8 + r] = __longlong_as_double((long long)raw);
             if (pre > 0) {
                 __syncwarp();
                 if (lane == 0) {
@@ -171,18 +182,23 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
     };
     // prologue: steps 0 .. P-1 (program chunk 0 first)
     mbar_wait(full, 0);
+    auto slot_arrive = [&](int sp) {
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(slotbar + sp % kIP))
+                     : "memory");
+    };
     for (int s = 0; s < kIP; ++s) {
         if (s < nsteps) {
             if (s > 0 && s % kISPC == 0) mbar_wait(full + ((s / kISPC) & (kINS - 1)), ((s / kISPC) / kINS) & 1);
             il_prefetch(rec_of(s), lane, val, dinv, rhs, zero, blk + (s % kIP) * kIBlk);
+            slot_arrive(s);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     for (int s = 0; s < nsteps; ++s) {
         const int* rec = rec_of(s);
         const int cnt = rec[0], need = rec[1];
         const int* br = rec + 4 + 6 * min(b, cnt - 1);
         const int I = br[0], myoff = br[1], off0 = br[4], off1 = br[5];
+        if (lane == 0) *cons = need;
         asm volatile(
             "{\n .reg .pred p;\n .reg .s32 r;\n"
             " setp.le.s32 p, %2, %0;\n"
@@ -193,8 +209,7 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
             : "+r"(have)
             : "r"(imp_a), "r"(need)
             : "memory");
-        asm volatile("cp.async.wait_group %0;" ::"n"(kIP - 1) : "memory");
-        __syncwarp();
+        mbar_wait(slotbar + s % kIP, (s / kIP) & 1);
         const double* sb = blk + (s % kIP) * kIBlk + b * 200;
         double acc = 0.0;
 #pragma unroll
@@ -224,10 +239,10 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
         if (sp < nsteps) {
             if (sp % kISPC == 0) mbar_wait(full + ((sp / kISPC) & (kINS - 1)), ((sp / kISPC) / kINS) & 1);
             il_prefetch(rec_of(sp), lane, val, dinv, rhs, zero, blk + (sp % kIP) * kIBlk);
+            slot_arrive(sp);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 }  // namespace
@@ -246,7 +261,7 @@ struct IlBuilt {
 };
 
 static int il_smem(int W, int hmax) {
-    return kINS * kLsCH + kIP * kIBlk * 8 + 2 * kINS * 8 + 16 + (8 * W + 16 + 8 * hmax) * 8;
+    return kINS * kLsCH + kIP * kIBlk * 8 + (2 * kINS + kIP) * 8 + 16 + (8 * W + 16 + 8 * std::min(hmax, kIH)) * 8;
 }
 
 static void il_build(const std::vector<int>& rp, const std::vector<int>& ci, const std::vector<int>& lev, int n,
@@ -329,11 +344,12 @@ static void il_build(const std::vector<int>& rp, const std::vector<int>& ci, con
     for (int g = 0; g < K; ++g) {
         const int* q = seq.data() + gstart[g];
         const auto& st = steps[g];
+        int run_need = 0;
         for (int k = 0; k + 1 < int(st.size()); ++k) {
             int* rec = reinterpret_cast<int*>(prog.data() + int64_t(gch[g].x + k / kISPC) * kIChunk +
                                               int64_t(k % kISPC) * kIStep);
             const int cnt = st[k + 1] - st[k];
-            int need = 0;
+            int need = 0, minneed = 1 << 30;
             rec[0] = cnt;
             for (int bb = 0; bb < kIB; ++bb) {
                 int* br = rec + 4 + 6 * bb;
@@ -353,13 +369,19 @@ static void il_build(const std::vector<int>& rp, const std::vector<int>& ci, con
                     if (gid[j] == g) {
                         br[4 + d] = 8 * (pos[j] & (W - 1));
                     } else {
-                        br[4 + d] = halo_off + 8 * hidx[j];
+                        br[4 + d] = halo_off + 8 * (hidx[j] & (kIH - 1));
                         need = std::max(need, hidx[j] + 1);
+                        minneed = std::min(minneed, hidx[j]);
                     }
                     ++d;
                 }
             }
+            // monotone per group (the importer's ring window follows it), and every
+            // entry a step reads must still be in the halo ring
+            need = std::max(need, run_need);
+            run_need = need;
             rec[1] = need;
+            if (minneed != (1 << 30) && need - minneed > kIH / 4) return;
         }
     }
     std::vector<int2> gimp(K);
