@@ -437,7 +437,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         build_band_order(c, L.n, sb.level.p, cl_R, L.border_b);
         return;
     }
-    const bool try_ls = L.glev_f && L.glev_b && L.n >= 2048;
+    const bool try_ls = L.glev_f && L.glev_b && L.n >= 512;
     // million-row levels: the level-synchronous program beats the band kernels by
     // 3-4x, so their schedules are not built and timed
     if (force.empty() && !try_cta && !try_seg && !try_cl && !try_ls) return;
@@ -490,8 +490,10 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
             cands = {148, 74, 37};
         else if (L.n >= 50000)
             cands = {74, 148, 37};
+        else if (L.n >= 8192)
+            cands = {37, 16, 8, 4};
         else
-            cands = {37, 16, 8};
+            cands = {16, 8, 4, 2, 1};  // small levels: one warp may beat any pipeline
         const bool first_fit = L.n >= 50000;  // large levels: the first program that fits
         for (int K : cands) {
             if (!build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) continue;
