@@ -1,6 +1,6 @@
 // blas.cu -- Ctx runtime + vector kernels of the Krylov loop (gmres.cpp:17-100):
-// deterministic fixed-order reductions (dot, norm), the fused MGS
-// dot/axpy step, scaling, multi-axpy, gathers and the stage combine.
+// deterministic fixed-order reductions (dot, norm), the re-orthogonalisation
+// gate, gathers and the stage combine (the Arnoldi passes are in gram.cu).
 //
 // Reductions are deterministic: the grid size is a function of n only, each
 // block reduces a fixed grid-stride slice through a fixed shared-memory tree,
@@ -175,43 +175,8 @@ __global__ void __launch_bounds__(kRT) k_dot(const double* a, const double* b, i
     finish(part, partials, ctr, out, nullptr, mode, sh);
 }
 
-// w -= (*hprev) * vprev ; partial of vcur . w  (vcur == w: squared norm)
-__global__ void __launch_bounds__(kRT) k_mgs(double* w, const double* vprev, const double* hprev,
-                                             const double* vcur, int64_t n, double* partials, unsigned* ctr,
-                                             double* hout, double* hsum, int mode, const int* gate) {
-    if (gate && *gate == 0) return;
-    __shared__ double sh[kRT];
-    const double h = vprev ? *hprev : 0.0;
-    double s = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)kRT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kRT) {
-        double wi = w[i];
-        if (vprev) {
-            wi = wi - h * vprev[i];
-            w[i] = wi;
-        }
-        if (vcur) s += vcur[i] * wi;
-    }
-    if (!vcur) return;
-    const double part = block_sum(s, sh);
-    __syncthreads();
-    finish(part, partials, ctr, hout, hsum, mode, sh);
-}
-
 __global__ void k_gate(const double* wnorm, const double* prenorm, int* gate) {
     *gate = (*wnorm < 0.7 * *prenorm) ? 1 : 0;
-}
-
-__global__ void k_div(double* y, const double* x, double a, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = x[i] / a;
-}
-
-__global__ void k_multi_axpy(double* z, const double* const* vt, const double* y, int k, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int j = 0; j < k; ++j) acc += y[j] * vt[j][i];
-        z[i] = acc;
-    }
 }
 
 __global__ void k_sub(double* out, const double* b, const double* ax, int64_t n) {
@@ -294,33 +259,10 @@ void nrm2(Ctx& c, const double* a, int64_t n, double* out) {
     check_launch("nrm2");
 }
 
-void mgs_step(Ctx& c, double* w, const double* vprev, const double* hprev, const double* vcur, int64_t n,
-              double* hout, bool accumulate, double* hsum, const int* gate) {
-    const bool self = (vcur == w);
-    double bytes = 8.0 * n * ((vprev ? 3 : 1) + (vcur && !self ? 1 : 0));
-    Ctx::Scope sc(&c, MPREC_K_MGS, bytes);
-    const int mode = self ? 1 : 0;
-    k_mgs<<<red_grid(n), kRT, 0, c.s>>>(w, vprev, hprev, vcur, n, c.red.p, c.red_ctr.p, hout,
-                                          accumulate ? hsum : nullptr, mode, gate);
-    check_launch("mgs_step");
-}
-
 void set_reorth_gate(Ctx& c, const double* wnorm, const double* prenorm, int* gate) {
     Ctx::Scope sc(&c, MPREC_K_BLAS1, 0.0);
     k_gate<<<1, 1, 0, c.s>>>(wnorm, prenorm, gate);
     check_launch("gate");
-}
-
-void div_scalar(Ctx& c, double* y, const double* x, double a, int64_t n) {
-    Ctx::Scope sc(&c, MPREC_K_BLAS1, 16.0 * n);
-    k_div<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(y, x, a, n);
-    check_launch("div");
-}
-
-void multi_axpy(Ctx& c, double* z, const double* const* vt, const double* y, int k, int64_t n) {
-    Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * n * (k + 1));
-    k_multi_axpy<<<grid_for(n, 256, c.sm_count * 8), 256, 0, c.s>>>(z, vt, y, k, n);
-    check_launch("multi_axpy");
 }
 
 void sub(Ctx& c, double* out, const double* b, const double* ax, int64_t n) {

@@ -112,7 +112,7 @@ struct Basis {
 
 struct Krylov {
     Basis V;
-    DBuf<double> w, t, vk, hcol, cre;
+    DBuf<double> w, t, vk, hcol;
     DBuf<double> ydev;
     DBuf<double*> ct;             // chunk pointer table
     DBuf<double> gt, pbuf, part;  // transposed Gram lower part, coefficients, pass-A partials
@@ -139,7 +139,6 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
     kr.w.ensure(n);
     kr.t.ensure(n);
     kr.hcol.ensure(max_it + 2);
-    kr.cre.ensure(max_it + 2);
     kr.vk.ensure(n);
     kr.ct.ensure(max_it / kBasisChunk + 2);
     kr.gt.ensure(size_t(max_it + 1) * (max_it + 1));
@@ -163,14 +162,12 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
         A(kr.t.p, kr.w.p);
         double* w = kr.w.p;
         double* hc = kr.hcol.p;
-        double* cr = kr.cre.p;
         // MGS (gmres.cpp:39-42) in Gram form (gram.cu): V^T w and the basis' new
         // Gram row in one pass, (I + L) h = V^T w, w -= V h in a second pass
         gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, false, k > 0, sc + 1, sc + 2, kr.part.p, nullptr);
         // one re-orthogonalisation pass when ||w|| < 0.7 pre_norm (gmres.cpp:44-50), gated on device
         set_reorth_gate(c, sc + 2, sc + 1, gate);
         gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, true, false, nullptr, sc + 3, kr.part.p, gate);
-        (void)cr;
         // read back the Hessenberg column
         MG_CUDA(cudaMemcpyAsync(col.data(), hc, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c.s));
         double tail[3];

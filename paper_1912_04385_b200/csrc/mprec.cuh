@@ -82,12 +82,6 @@ void copy(Ctx& c, double* y, const double* x, int64_t n);
 void dot(Ctx& c, const double* a, const double* b, int64_t n, double* out_dev);
 // out_dev <- ||a||_2
 void nrm2(Ctx& c, const double* a, int64_t n, double* out_dev);
-// MGS step of gmres.cpp:39-50, fused:
-//   if (gate == nullptr || *gate) { if (vprev) w -= (*hprev_scale) * vprev;
-//                                   if (vcur) *hout = vcur . w (+= if accumulate) }
-// hprev is read from device memory (the previous dot), so no host sync.
-void mgs_step(Ctx& c, double* w, const double* vprev, const double* hprev, const double* vcur,
-              int64_t n, double* hout, bool accumulate, double* hsum, const int* gate);
 // Gram-form MGS sweep (gram.cu): with the basis v_0..v_k (device pointer table
 // vt), h = (I + L)^-1 V^T w (h += when accumulate), w -= V h; gt (ld x ld,
 // transposed Gram lower part) gains the row of v_k when want_q; pre_norm =
@@ -107,10 +101,6 @@ void gram_sweep(Ctx& c, const double* const* vt, int k, double* w, int64_t n, do
                 const int* gate);
 // gate_dev <- (||w|| < 0.7 * pre_norm) evaluated on device scalars
 void set_reorth_gate(Ctx& c, const double* wnorm, const double* prenorm, int* gate);
-// y = x / alpha (host scalar)
-void div_scalar(Ctx& c, double* y, const double* x, double alpha, int64_t n);
-// z = sum_i y[i] * V[i] (device pointer table, host-provided coefficients)
-void multi_axpy(Ctx& c, double* z, const double* const* vtab_dev, const double* y_dev, int k, int64_t n);
 // out = b - ax ; optional
 void sub(Ctx& c, double* out, const double* b, const double* ax, int64_t n);
 // out[c] = x[c*stride + f]
