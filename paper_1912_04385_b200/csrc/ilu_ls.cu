@@ -12,11 +12,13 @@
 // with the packed inverses of the diagonal blocks (k_ilu_dinv8).  The block
 // values are NOT copied into the program (they are the 10 GB factor): the
 // compute warp prefetches the blocks of the step P = 20 steps ahead straight
-// from the factor with cp.async (16-byte chunks; completion tracked by one
-// mbarrier per ring slot via cp.async.mbarrier.arrive) into a shared-memory
-// ring, so HBM latency leaves the dependency chain.  The import halo is a ring
+// from the factor with 1-D TMA bulk copies (one per 512-byte block, completion
+// counted on one mbarrier per ring slot) into a shared-memory ring, so HBM
+// latency leaves the dependency chain.  The import halo is a ring
 // of 256 block rows; the importer is held back by the consumer's progress.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -61,37 +63,40 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_relaxed_il(const double* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
-// prefetch the blocks of one step into a ring slot: per block row b,
-// [0, 64) first dependency block, [64, 128) second, [128, 192) packed inverse of
-// the diagonal block, [192, 200) right-hand side.  Missing dependencies read the
-// zero block; padding block rows read the step's first block row.
+// prefetch the blocks of one step into a ring slot with 1-D TMA bulk copies
+// (16 per step, lanes 0..15, completion counted on the slot's mbarrier): per
+// block row b, [0, 64) first dependency block, [64, 128) second, [128, 192) packed
+// inverse of the diagonal block, [192, 200) right-hand side.  Missing
+// dependencies read the zero block; padding block rows read the step's first
+// block row.  (16-byte cp.async per lane stalled at issue: 1.5 us per step.)
 __device__ __forceinline__ void il_prefetch(const int* rec, int lane, const double* __restrict__ val,
                                             const double* __restrict__ dinv, const double* __restrict__ rhs,
-                                            const double* __restrict__ zero, double* slot) {
-    const int cnt = rec[0];
-    for (int q = lane; q < kIB * 100; q += 32) {
-        const int b = q / 100, w = q - b * 100;
+                                            const double* __restrict__ zero, double* slot, uint64_t* bar) {
+    if (lane == 0) mbar_expect_tx(bar, kIB * (3 * 512 + 64));
+    __syncwarp();
+    if (lane < 16) {
+        const int cnt = rec[0];
+        const int b = lane >> 2, w = lane & 3;
         const int* br = rec + 4 + 6 * min(b, cnt - 1);
         const int I = br[0];
         const double* src;
-        if (w < 64) {
-            const int k = br[2 + (w >> 5)];
-            src = (k >= 0 ? val + int64_t(k) * 64 : zero) + 2 * (w & 31);
-        } else if (w < 96) {
-            src = dinv + int64_t(I) * 64 + 2 * (w - 64);
+        unsigned bytes = 512;
+        if (w < 2) {
+            const int k = br[2 + w];
+            src = k >= 0 ? val + int64_t(k) * 64 : zero;
+        } else if (w == 2) {
+            src = dinv + int64_t(I) * 64;
         } else {
-            src = rhs + int64_t(I) * 8 + 2 * (w - 96);
+            src = rhs + int64_t(I) * 8;
+            bytes = 64;
         }
-        cp16(slot + b * 200 + 2 * w, src);
+        bulk_g2s(slot + b * 200 + 64 * w, src, bytes, bar);
     }
 }
 
@@ -101,7 +106,8 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
                                                           const double* __restrict__ val,
                                                           const double* __restrict__ dinv,
                                                           const double* __restrict__ rhs,
-                                                          const double* __restrict__ zero, double* y, int W) {
+                                                          const double* __restrict__ zero, double* y, int W,
+                                                          long long* stats) {
     extern __shared__ __align__(128) unsigned char sm[];
     char* ring = reinterpret_cast<char*>(sm);                             // program chunks
     double* blk = reinterpret_cast<double*>(sm + kINS * kLsCH);           // prefetched blocks
@@ -120,7 +126,7 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
         }
-        for (int s = 0; s < kIP; ++s) mbar_init(slotbar + s, 32);
+        for (int s = 0; s < kIP; ++s) mbar_init(slotbar + s, 1);
         *imported = 0;
         *cons = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -173,6 +179,8 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
     }
     // compute warp
     if (nsteps == 0) return;
+    long long t_start = 0, t_imp = 0, t_blk = 0;
+    if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     const int b = lane >> 3, r = lane & 7;
     const unsigned imp_a = smem_u32(imported);
     const volatile double* vxs = xs;
@@ -182,15 +190,10 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
     };
     // prologue: steps 0 .. P-1 (program chunk 0 first)
     mbar_wait(full, 0);
-    auto slot_arrive = [&](int sp) {
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(slotbar + sp % kIP))
-                     : "memory");
-    };
     for (int s = 0; s < kIP; ++s) {
         if (s < nsteps) {
             if (s > 0 && s % kISPC == 0) mbar_wait(full + ((s / kISPC) & (kINS - 1)), ((s / kISPC) / kINS) & 1);
-            il_prefetch(rec_of(s), lane, val, dinv, rhs, zero, blk + (s % kIP) * kIBlk);
-            slot_arrive(s);
+            il_prefetch(rec_of(s), lane, val, dinv, rhs, zero, blk + (s % kIP) * kIBlk, slotbar + s % kIP);
         }
     }
     for (int s = 0; s < nsteps; ++s) {
@@ -199,6 +202,8 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
         const int* br = rec + 4 + 6 * min(b, cnt - 1);
         const int I = br[0], myoff = br[1], off0 = br[4], off1 = br[5];
         if (lane == 0) *cons = need;
+        long long ta = 0, tb = 0, tc = 0;
+        if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
         asm volatile(
             "{\n .reg .pred p;\n .reg .s32 r;\n"
             " setp.le.s32 p, %2, %0;\n"
@@ -209,7 +214,13 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
             : "+r"(have)
             : "r"(imp_a), "r"(need)
             : "memory");
+        if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb));
         mbar_wait(slotbar + s % kIP, (s / kIP) & 1);
+        if (stats) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tc));
+            t_imp += tb - ta;
+            t_blk += tc - tb;
+        }
         const double* sb = blk + (s % kIP) * kIBlk + b * 200;
         double acc = 0.0;
 #pragma unroll
@@ -236,13 +247,25 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
         if (s % kISPC == kISPC - 1 && lane == 0) mbar_arrive(empty + ((s / kISPC) & (kINS - 1)));
         // prefetch step s + P (its program chunk may be the next one)
         const int sp = s + kIP;
+        long long td = 0, te = 0;
+        if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(td));
         if (sp < nsteps) {
             if (sp % kISPC == 0) mbar_wait(full + ((sp / kISPC) & (kINS - 1)), ((sp / kISPC) / kINS) & 1);
-            il_prefetch(rec_of(sp), lane, val, dinv, rhs, zero, blk + (sp % kIP) * kIBlk);
-            slot_arrive(sp);
+            il_prefetch(rec_of(sp), lane, val, dinv, rhs, zero, blk + (sp % kIP) * kIBlk, slotbar + sp % kIP);
+        }
+        if (stats) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
+            t_imp += (te - td) << 32;  // prefetch issue time in the high word
         }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (stats && lane == 0) {
+        long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        stats[4 * g] = t_start;
+        stats[4 * g + 1] = t_end;
+        stats[4 * g + 2] = t_imp;
+        stats[4 * g + 3] = t_blk;
+    }
 }
 
 }  // namespace
@@ -445,13 +468,27 @@ void ilu_ls_solve(Ctx& c, const IluLs& s, const IluLs& zero_owner, bool fwd, con
             MG_CUDA(cudaFuncSetAttribute(k_ilu_ls<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
         attr[fwd] = true;
     }
+    static const bool want_stats = getenv("MPREC_ILU_LS_STATS") != nullptr;
+    DBuf<long long> st;
+    if (want_stats) st.alloc(4 * s.K);
     if (fwd)
         k_ilu_ls<true><<<s.K, kIThreads, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, val, dinv, rhs,
-                                                        zero_owner.zero.p, y, s.W);
+                                                        zero_owner.zero.p, y, s.W, st.p);
     else
         k_ilu_ls<false><<<s.K, kIThreads, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, val, dinv, rhs,
-                                                         zero_owner.zero.p, y, s.W);
+                                                         zero_owner.zero.p, y, s.W, st.p);
     check_launch(fwd ? "ilu ls fwd" : "ilu ls bwd");
+    if (want_stats) {
+        auto h = st.to_host(c.s);
+        long long t0 = h[0];
+        for (int g = 0; g < s.K; ++g) t0 = std::min(t0, h[4 * g]);
+        fprintf(stderr, "[ilu ls %s] K=%d steps=%d (group: start end import_wait_us block_wait_us)\n", fwd ? "fwd" : "bwd",
+                s.K, s.nsteps);
+        for (int g = 0; g < s.K; g += std::max(1, s.K / 10))
+            fprintf(stderr, "  g%3d %9.1f %9.1f import %9.1f prefetch-issue %9.1f block %9.1f\n", g,
+                    (h[4 * g] - t0) * 1e-3, (h[4 * g + 1] - t0) * 1e-3, (h[4 * g + 2] & 0xffffffffll) * 1e-3,
+                    (h[4 * g + 2] >> 32) * 1e-3, h[4 * g + 3] * 1e-3);
+    }
 }
 
 }  // namespace mg
