@@ -165,18 +165,21 @@ __global__ void k_invd(const double* v, const int* diag, int n, double* invd) {
     if (i < n) invd[i] = 1.0 / v[diag[i]];
 }
 
-// 8 lanes per row; mode 0: y = Ax, 1: y = b - Ax, 2: y = y + Ax
+// LN lanes per row (chosen per matrix from its mean row length: short P rows
+// and 5-point level-0 rows waste most of 8 lanes); mode 0: y = Ax, 1: y = b - Ax,
+// 2: y = y + Ax
+template <int LN>
 __global__ void __launch_bounds__(256) k_csr(const int* __restrict__ rp, const int* __restrict__ ci,
                                              const double* __restrict__ v, const double* __restrict__ x, double* y,
                                              const double* __restrict__ b, int n, int mode) {
     const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
-    const int row = int(g >> 3), s = int(g & 7);
+    const int row = int(g / LN), s = int(g % LN);
     double acc = 0.0;
     if (row < n)
-        for (int k = rp[row] + s; k < rp[row + 1]; k += 8) acc += __ldg(v + k) * __ldg(x + __ldg(ci + k));
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        for (int k = __ldg(rp + row) + s; k < __ldg(rp + row + 1); k += LN)
+            acc += __ldg(v + k) * __ldg(x + __ldg(ci + k));
+#pragma unroll
+    for (int o = 1; o < LN; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (row < n && s == 0) y[row] = mode == 0 ? acc : (mode == 1 ? b[row] - acc : y[row] + acc);
 }
 
@@ -272,8 +275,16 @@ void csr_spmv(Ctx& c, const CsrView& a, const double* x, double* y, const double
     const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 8.0 * a.m + 8.0 * a.n + ((b || add_to_y) ? 8.0 * a.n : 0.0);
     Ctx::Scope sc(&c, kclass, bytes);
     const int mode = add_to_y ? 2 : (b ? 1 : 0);
-    const int64_t threads = (int64_t)a.n * 8;
-    k_csr<<<int((threads + 255) / 256), 256, 0, c.s>>>(a.rp, a.ci, a.v, x, y, b, a.n, mode);
+    const double per_row = double(a.nnz) / std::max(a.n, 1);
+    const int ln = per_row <= 3.0 ? 2 : per_row <= 6.0 ? 4 : per_row <= 12.0 ? 8 : 16;
+    const int64_t threads = (int64_t)a.n * ln;
+    const int grid = int((threads + 255) / 256);
+    switch (ln) {
+        case 2: k_csr<2><<<grid, 256, 0, c.s>>>(a.rp, a.ci, a.v, x, y, b, a.n, mode); break;
+        case 4: k_csr<4><<<grid, 256, 0, c.s>>>(a.rp, a.ci, a.v, x, y, b, a.n, mode); break;
+        case 8: k_csr<8><<<grid, 256, 0, c.s>>>(a.rp, a.ci, a.v, x, y, b, a.n, mode); break;
+        default: k_csr<16><<<grid, 256, 0, c.s>>>(a.rp, a.ci, a.v, x, y, b, a.n, mode); break;
+    }
     check_launch("csr_spmv");
 }
 
