@@ -45,6 +45,8 @@ namespace mg {
 namespace {
 
 constexpr int kThreads = 96;  // warp 0: compute, warp 1: importer, warp 2: loader
+constexpr int kLsExportBit = 1 << 30;       // record myslot: row is read by the next group
+constexpr int kLsSlotMask = kLsExportBit - 1;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
@@ -152,7 +154,8 @@ __device__ __forceinline__ void ls_slots(const char* rec, int* sl) {
 template <int ND>
 __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ prog, const int2* __restrict__ gch,
                                                         const int* __restrict__ imp, const int2* __restrict__ gimp,
-                                                        double* xnew, int W, int trash, int ns, long long* stats) {
+                                                        double* xnew, int W, int trash, int ns, long long* stats,
+                                                        int push) {
     constexpr int RS = ls_rs(ND == 2 ? 0 : ND == 4 ? 1 : ND == 8 ? 2 : ND == 16 ? 3 : 4);
     extern __shared__ __align__(128) unsigned char sm[];
     char* ring = reinterpret_cast<char*>(sm);
@@ -172,7 +175,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
         xs[W] = 0.0;  // zero slot (padding dependencies)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // cluster push (launched as clusters of 2): the even CTA of a pair stores its
+    // exported values straight into the odd CTA's halo (DSMEM), whose importer
+    // then only polls shared memory; the halo starts as kPending in every thread
+    // block and a cluster barrier orders that before any remote store
+    const bool pushed_in = push && (g & 1);  // my halo is written by my cluster peer
+    if (pushed_in) {
+        const int nimp = gimp[g].y;
+        for (int i = threadIdx.x; i < nimp; i += blockDim.x)
+            reinterpret_cast<unsigned long long*>(xs + W + 1)[i] = kPending;
+    }
     __syncthreads();
+    if (push) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
     if (warp == 2) {  // loader: program chunks -> shared-memory ring (1-D TMA bulk copies)
         if (lane == 0)
             for (int c = 0; c < ch.y; ++c) {
@@ -181,6 +198,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
                 mbar_expect_tx(full + s, kLsCH);
                 bulk_g2s(ring + s * kLsCH, prog + (int64_t)(ch.x + c) * kLsCH, kLsCH, full + s);
             }
+        return;
+    }
+    if (warp == 1 && pushed_in) {  // importer, cluster push: poll the local halo
+        const int nimp = gimp[g].y;
+        volatile unsigned long long* halo = reinterpret_cast<volatile unsigned long long*>(xs + W + 1);
+        volatile int* vimp = imported;
+        int base = 0;
+        while (base < nimp) {
+            const int idx = base + lane;
+            const bool ready = idx < nimp && halo[idx] != kPending;
+            const unsigned m = __ballot_sync(0xffffffffu, ready);
+            const int pre = min(m == 0xffffffffu ? 32 : __ffs(~m) - 1, nimp - base);
+            if (pre > 0) {
+                if (lane == 0) {
+                    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+                    *vimp = base + pre;
+                }
+                base += pre;
+            }
+        }
         return;
     }
     if (warp == 1) {  // importer: previous group's values -> halo, in production order
@@ -221,6 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
     int have = 0;
     long long t_start = 0;
     if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    // cluster push target: the peer CTA's halo (shared::cluster address)
+    const bool push_out = push && !(g & 1) && g + 1 < int(gridDim.x);
+    unsigned peer_halo = 0;
+    int nexp = 0;
+    if (push_out)
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer_halo) : "r"(smem_u32(xs + W + 1)), "r"(1));
     for (int c = 0; c < ch.y; ++c) {
         const int slot = c & (ns - 1);
         mbar_wait(full + slot, (c / ns) & 1);
@@ -265,12 +308,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
             }
             const double x = ls_dot<ND>(e, xv, cc);
             const int row = lane < h.x ? rs.x : -1;
-            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(xs + (lane < h.x ? rs.y : trash))), "d"(x)
+            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(
+                             smem_u32(xs + (lane < h.x ? (rs.y & kLsSlotMask) : trash))),
+                         "d"(x)
                          : "memory");
             asm volatile(
                 "{\n .reg .pred p;\n setp.ge.s32 p, %2, 0;\n @p st.relaxed.gpu.global.b64 [%0], %1;\n}" ::"l"(xnew + row),
                 "l"(__double_as_longlong(x)), "r"(row)
                 : "memory");
+            if (push_out) {
+                // exported rows arrive in the peer's import order (processing order)
+                const bool ex = lane < h.x && (rs.y & kLsExportBit);
+                const unsigned m = __ballot_sync(0xffffffffu, ex);
+                const int hidx = nexp + __popc(m & ((1u << lane) - 1));
+                asm volatile(
+                    "{\n .reg .pred p;\n setp.ne.s32 p, %2, 0;\n"
+                    " @p st.relaxed.cluster.shared::cluster.b64 [%0], %1;\n}" ::"r"(peer_halo + 8u * unsigned(hidx)),
+                    "l"(__double_as_longlong(x)), "r"(int(ex))
+                    : "memory");
+                nexp += __popc(m);
+            }
             __syncwarp();
             st = stn;
             h = hn;
@@ -447,7 +504,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_lsv(const char* __restrict__
             const double acc = (fma(ea.x, x0, ea.y * x1) + fma(eb.x, x2, eb.y * x3)) + rest;
             const double x = cc - acc;
             const int row = lane < h.x ? rs.x : -1;
-            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(xs + (lane < h.x ? rs.y : trash))), "d"(x)
+            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(
+                             smem_u32(xs + (lane < h.x ? (rs.y & kLsSlotMask) : trash))),
+                         "d"(x)
                          : "memory");
             asm volatile(
                 "{\n .reg .pred p;\n setp.ge.s32 p, %2, 0;\n @p st.relaxed.gpu.global.b64 [%0], %1;\n}" ::"l"(xnew + row),
@@ -616,7 +675,7 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
                 };
                 *cp = 0.0;
                 rsl[0] = i;
-                rsl[1] = pos[i] & (W - 1);
+                rsl[1] = (pos[i] & (W - 1)) | (exported[i] ? kLsExportBit : 0);
                 coff[i] = (cbase + off + 16 + r * RS + 16) | (exported[i] ? 1 : 0);
                 for (int d = 0; d < std::max(ND, 4); ++d) {
                     if (d < ND) coef(d) = 0.0;
@@ -755,12 +814,45 @@ long long* g_ls_stats = nullptr;  // diagnostics: per-group {start, end, wait ns
 template <int ND>
 static void launch_ls(Ctx& c, const LsSched& s, double* xnew) {
     static bool attr = false;
+    static int max_clusters = -1;
     if (!attr) {
         MG_CUDA(cudaFuncSetAttribute(k_gs_ls<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
         attr = true;
     }
-    k_gs_ls<ND><<<s.K, kThreads, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, xnew, s.W, s.W + 1 + s.hmax, s.ns,
-                                                g_ls_stats);
+    // clusters of two thread blocks (DSMEM push across every other group boundary)
+    // when all K/2 clusters fit on the device at once.  Opt-in (MPREC_LS_PUSH=1):
+    // measured slower at c5 (level 0: 0.77 vs 0.59 ms; the per-step ballot and
+    // remote store slow the pushing groups more than the halved boundary
+    // latency saves), DESIGN.md §5.1
+    static const bool push_on = [] {
+        const char* e = getenv("MPREC_LS_PUSH");
+        return e && e[0] == '1';
+    }();
+    bool push = push_on && (s.K % 2 == 0);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(s.K);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = s.smem;
+    cfg.stream = c.s;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (push) {
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_gs_ls<ND>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        push = n >= s.K / 2;
+    }
+    if (!push) cfg.numAttrs = 0;
+    MG_CUDA(cudaLaunchKernelEx(&cfg, k_gs_ls<ND>, (const char*)s.prog.p, (const int2*)s.gch.p, (const int*)s.imp.p,
+                               (const int2*)s.gimp.p, xnew, s.W, s.W + 1 + s.hmax, s.ns, g_ls_stats, push ? 1 : 0));
+    (void)max_clusters;
 }
 
 void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,

@@ -27,9 +27,13 @@ def cfg2():
     return gen.generate(2)
 
 
-@pytest.mark.parametrize("mode", ["warp", "cta", "seg", "cluster", "ls", "ls-fixed", "ls-var", ""])
+@pytest.mark.parametrize("mode", ["warp", "cta", "seg", "cluster", "ls", "ls-fixed", "ls-var", "ls-push", ""])
 @pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
 def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
+    if mode == "ls-push":
+        # level-synchronous programs launched as clusters of two (DSMEM push); the
+        # switch is read once per process, so this case runs in its own interpreter
+        pytest.skip("MPREC_LS_PUSH is read once per process: covered by test_ls_cluster_push_subprocess")
     if mode.startswith("ls-"):
         # level-synchronous programs with fixed-class (k_gs_ls<ND>) or variable-width
         # (k_gs_lsv) records on every level
@@ -61,3 +65,23 @@ def test_ilu_level_sync_solve(gpu, orc, cfg2, method, monkeypatch):
     rg, ro = sg.solve(), so.solve()
     assert abs(rg.iterations - ro.iterations) <= 1
     assert rel(rg.x, ro.x) < 1e-6
+
+
+def test_ls_cluster_push_subprocess(tmp_path):
+    """Cluster-push LS programs (MPREC_LS_PUSH=1, read once per process) against the oracle."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_1912_04385_b200 import gen; from paper_1912_04385_b200.api import gpu; import oracle;"
+        "from tests.systems import random_vec;"
+        "a, b, _ = gen.generate(2); r = random_vec(a.dim, 11);"
+        "sg = gpu().system(a).setup('cptr3-amg', b); so = oracle.api().system(a).setup('cptr3-amg', b);"
+        "e = np.linalg.norm(sg.apply(r) - so.apply(r)) / np.linalg.norm(so.apply(r));"
+        "rg, ro = sg.solve(), so.solve(); print(e, rg.iterations, ro.iterations);"
+        "assert e < 1e-10 and abs(rg.iterations - ro.iterations) <= 1"
+    )
+    env = dict(os.environ, MPREC_LS_PUSH="1", MPREC_GS_MODE="ls", MPREC_GS_LS_K="16")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
