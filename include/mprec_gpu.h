@@ -58,6 +58,22 @@ typedef struct mprec_amg_params {
     int max_levels;            /* 25   */
 } mprec_amg_params;
 
+/* ScalingOptions (proj/include/mprec/scaling.hpp:22-30): the square D factors
+ * of the left scaling are the full per-cell block (BLOCK) or its scalar
+ * diagonal (SCALAR, BlockMatrix::block_diagonal_of block_matrix.cpp:186-193);
+ * CPTR3's second scaling divides by the diagonal of the post-step-1 B_PP
+ * (default) or of the original A_PP (second_scaling_from_original = 1,
+ * scaling.cpp:126). */
+typedef enum mprec_diag_mode {
+    MPREC_DIAG_BLOCK = 0,
+    MPREC_DIAG_SCALAR = 1,
+} mprec_diag_mode;
+
+typedef struct mprec_scaling_options {
+    int diag_mode;                    /* mprec_diag_mode, default BLOCK */
+    int second_scaling_from_original; /* default 0 */
+} mprec_scaling_options;
+
 /* Uniform-layout BlockMatrix (proj/include/mprec/block_matrix.hpp:50-101):
  * n_cells block rows, nb unknowns per cell in (s..., P, T) order
  * (field_layout.hpp:62-66), block columns sorted ascending per row with the
@@ -91,6 +107,11 @@ typedef struct mprec_solve_result {
     double setup_s;             /* left_scale + build_preconditioner */
     double solve_s;             /* all GMRES attempts */
     int total_iterations;       /* summed over all attempts */
+    /* per tolerance-tightening attempt (harness.cpp:209-217), index < attempts */
+    int attempt_iterations[3];
+    int attempt_converged[3];        /* GMRES' own convergence flag */
+    double attempt_tol[3];           /* the GMRES tolerance of the attempt */
+    double attempt_true_residual[3]; /* residual_check on the original system */
 } mprec_solve_result;
 
 /* GlobalJacobian (condense.hpp:64-81) in plain arrays.  Primary blocks are
@@ -137,6 +158,16 @@ int mprec_gpu_create(const mprec_bsr* a, mprec_gpu_system** out);
  * NULL (defaults).  b: host rhs (n_cells*nb). */
 int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg,
                     const double* b);
+
+/* Same with explicit ScalingOptions (scaling.hpp:22-30, left_scale's 4th
+ * argument, scaling.cpp:149-158); opts may be NULL (defaults). */
+int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params* amg,
+                         const mprec_scaling_options* opts, const double* b);
+
+/* ScaledSystem::scaling_record joined with ", " as SolveOutcome::scaling_record
+ * (harness.cpp:197-201), e.g. "[D_Ps;D_Ts]*D_ss^-1, D_Tp*D_PP^-1"; truncated
+ * to cap-1 characters, always NUL-terminated. */
+int mprec_gpu_scaling_record(mprec_gpu_system* h, char* buf, int cap);
 
 /* StagePreconditioner::apply (stages.cpp:36-59) / apply_stage (stages.hpp:54). */
 int mprec_gpu_apply(mprec_gpu_system* h, const double* r, double* z);

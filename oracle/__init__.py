@@ -29,3 +29,23 @@ def api():
             f.restype = _C.c_int
             f.argtypes = args
     return _api
+
+
+REF_LIB = _os.path.join(_HERE, "_ref", "libmprec_ref.so")
+_ref_api = None
+
+
+def ref_available() -> bool:
+    return _os.path.exists(REF_LIB)
+
+
+def ref_api():
+    """Api bound to oracle/_ref/libmprec_ref.so (prefix ref_): the reference's
+    own sources compiled against the Eigen-subset shim (oracle/Makefile `ref`)."""
+    global _ref_api
+    if _ref_api is None:
+        from paper_1912_04385_b200.api import Api
+        if not ref_available():
+            raise ImportError(f"{REF_LIB} missing: run `make -C oracle ref` where /root/reference exists")
+        _ref_api = Api(REF_LIB, "ref_")
+    return _ref_api

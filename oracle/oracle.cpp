@@ -154,16 +154,22 @@ int Bsr::find_block(int row, int col) const {
     return -1;
 }
 
-// block_matrix.cpp:103-114; the per-block gemv is restated column by column.
+// block_matrix.cpp:103-114.
 Vec Bsr::apply_block(const Vec& x) const {
     if (int64_t(x.size()) != int64_t(dim())) throw Error(DIMENSION, "spmv length mismatch");
+    // yc += B_k * x_k: the block product is summed over the block's columns
+    // from the first term into a temporary, then added (the product convention
+    // of the Eigen call sites, oracle/eigen_shim/shim.hpp).
     Vec y(size_t(dim()), 0.0);
     for (int c = 0; c < nc; ++c) {
         double* yc = &y[size_t(c) * nb];
         for (int k = rp[c]; k < rp[c + 1]; ++k) {
             const double* xs = &x[size_t(ci[k]) * nb];
-            for (int col = 0; col < nb; ++col)
-                for (int r = 0; r < nb; ++r) yc[r] += at(k, r, col) * xs[col];
+            for (int r = 0; r < nb; ++r) {
+                double acc = at(k, r, 0) * xs[0];
+                for (int col = 1; col < nb; ++col) acc += at(k, r, col) * xs[col];
+                yc[r] += acc;
+            }
         }
     }
     return y;
@@ -741,10 +747,12 @@ void combine_cell(Bsr& a, Vec& b, int c, const std::vector<int>& tl, const std::
 }
 
 // scaling_factors (scaling.cpp:31-46) for target fields tl, source fields sl,
-// DiagMode::Block, evaluated on `a`.  Throws SingularBlock(cell, what) at the
-// first cell (ascending) whose D_ss fails the pivot check.
+// evaluated on `a`: D_ts is the full cell block, D_ss the block or (scalar_diag,
+// DiagMode::Scalar, block_matrix.cpp:186-193) its diagonal.  Throws
+// SingularBlock(cell, what) at the first cell (ascending) whose D_ss fails the
+// pivot check.
 std::vector<Vec> scaling_factors(const Bsr& a, const std::vector<int>& tl, const std::vector<int>& sl,
-                                 const char* what) {
+                                 const char* what, bool scalar_diag) {
     const int nt = int(tl.size()), ns = int(sl.size());
     std::vector<Vec> w(a.nc);
     if (ns == 0) {
@@ -756,7 +764,7 @@ std::vector<Vec> scaling_factors(const Bsr& a, const std::vector<int>& tl, const
         const int d = a.dpos[c];
         Vec dss(size_t(ns) * ns);
         for (int j = 0; j < ns; ++j)
-            for (int i = 0; i < ns; ++i) dss[size_t(j) * ns + i] = a.at(d, sl[i], sl[j]);
+            for (int i = 0; i < ns; ++i) dss[size_t(j) * ns + i] = (scalar_diag && i != j) ? 0.0 : a.at(d, sl[i], sl[j]);
         if (!invert_block(dss, ns, inv[c]))
             throw Error(SINGULAR_BLOCK, std::string("singular ") + what + " block in cell " + std::to_string(c), c);
     }
@@ -773,7 +781,7 @@ std::vector<Vec> scaling_factors(const Bsr& a, const std::vector<int>& tl, const
 }  // namespace
 
 // scaling.cpp:73-88 (CPR) / :107-147 (CPTR3) / :149-158 (dispatch)
-ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m) {
+ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m, const ScalingOptions& o) {
     if (int64_t(b.size()) != int64_t(a.dim())) throw Error(DIMENSION, "rhs length mismatch");
     if (a.nb < 2 && m != Method::Ilu0) throw Error(DIMENSION, "CPR/CPTR3 need P and T unknowns (nb >= 2)");
     ScaledSystem s;
@@ -785,7 +793,7 @@ ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m) {
     std::vector<int> S;
     for (int k = 0; k < ns; ++k) S.push_back(k);
     if (m == Method::CptrDirect) {  // scaling.cpp:90-105
-        const auto w = scaling_factors(a, {P, T}, S, "D_ss");
+        const auto w = scaling_factors(a, {P, T}, S, "D_ss", o.scalar_diag);
         for (int c = 0; c < a.nc; ++c) combine_cell(s.a_bar, s.b_bar, c, {P, T}, S, w[c]);
         s.scaling_record.push_back("D_es*D_ss^-1");
         s.b_ee = extract_pt(s.a_bar);
@@ -794,22 +802,24 @@ ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m) {
     if (m == Method::Cpr || m == Method::CprDirect) {
         std::vector<int> h = S;
         h.push_back(T);
-        const auto w = scaling_factors(a, {P}, h, "D_hh");
+        const auto w = scaling_factors(a, {P}, h, "D_hh", o.scalar_diag);
         for (int c = 0; c < a.nc; ++c) combine_cell(s.a_bar, s.b_bar, c, {P}, h, w[c]);
         s.scaling_record.push_back("D_Ph*D_hh^-1");
         s.b_pp = s.a_bar.extract_field(P);
         return s;
     }
     if (m == Method::Cptr3 || m == Method::Cptr3Direct) {
-        const auto w1 = scaling_factors(a, {P, T}, S, "D_ss");
+        const auto w1 = scaling_factors(a, {P, T}, S, "D_ss", o.scalar_diag);
         for (int c = 0; c < a.nc; ++c) combine_cell(s.a_bar, s.b_bar, c, {P, T}, S, w1[c]);
         s.scaling_record.push_back("[D_Ps;D_Ts]*D_ss^-1");
-        // second scaling: D_Tp * D_PP^-1 on the once-scaled matrix
+        // second scaling: D_Tp (once-scaled) * D_PP^-1, D_PP of the once-scaled
+        // matrix or, with second_scaling_from_original, of A (scaling.cpp:126)
+        const Bsr& pp_source = o.second_scaling_from_original ? a : s.a_bar;
         std::vector<Vec> w2(a.nc);
         for (int c = 0; c < a.nc; ++c) {
             const int d = s.a_bar.dpos[c];
             Vec inv;
-            if (!invert_block(Vec{s.a_bar.at(d, P, P)}, 1, inv))
+            if (!invert_block(Vec{pp_source.at(pp_source.dpos[c], P, P)}, 1, inv))
                 throw Error(SINGULAR_BLOCK, "singular D_PP block in cell " + std::to_string(c), c);
             w2[c] = Vec{s.a_bar.at(d, T, P) * inv[0]};
         }

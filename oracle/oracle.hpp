@@ -174,7 +174,13 @@ struct ScaledSystem {
     std::vector<std::string> scaling_record;
 };
 
-ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m);  // scaling.cpp:149-158
+// ScalingOptions (scaling.hpp:22-30)
+struct ScalingOptions {
+    bool scalar_diag = false;                   // DiagMode::Scalar for the square D factors
+    bool second_scaling_from_original = false;  // CPTR3 step 2 divides by the original A_PP
+};
+
+ScaledSystem left_scale(const Bsr& a, const Vec& b, Method m, const ScalingOptions& o = {});  // scaling.cpp:149-158
 
 struct Stage {
     enum Kind { AMG, DIRECT, ILU } kind = ILU;

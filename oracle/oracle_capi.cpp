@@ -99,20 +99,42 @@ int orc_create(const mprec_bsr* a, orc_system** out) {
     });
 }
 
-int orc_setup(orc_system* h, int method, const mprec_amg_params* amg, const double* b) {
+int orc_setup_opts(orc_system* h, int method, const mprec_amg_params* amg, const mprec_scaling_options* so,
+                   const double* b) {
     return guard([&] {
         if (!b) {
             if (int64_t(h->b_ingested.size()) != int64_t(h->a.dim())) throw Error(DIMENSION, "no rhs");
             b = h->b_ingested.data();
         }
         if (method < 0 || method > 5) throw Error(CONFIG, "unknown method id " + std::to_string(method));
+        ScalingOptions o;
+        if (so) {
+            o.scalar_diag = so->diag_mode == MPREC_DIAG_SCALAR;
+            o.second_scaling_from_original = so->second_scaling_from_original != 0;
+        }
         h->ready = false;
         h->b.assign(b, b + h->a.dim());
         const double t0 = now_s();
-        h->sc = left_scale(h->a, h->b, Method(method));
+        h->sc = left_scale(h->a, h->b, Method(method), o);
         h->prec = build_preconditioner(h->sc, to_params(amg));
         h->setup_s = now_s() - t0;
         h->ready = true;
+    });
+}
+
+int orc_setup(orc_system* h, int method, const mprec_amg_params* amg, const double* b) {
+    return orc_setup_opts(h, method, amg, nullptr, b);
+}
+
+int orc_scaling_record(orc_system* h, char* buf, int cap) {
+    return guard([&] {
+        if (!h->ready) throw Error(SETUP, "setup not done");
+        std::string s;
+        for (const std::string& r : h->sc.scaling_record) s += (s.empty() ? "" : ", ") + r;
+        if (cap > 0) {
+            std::strncpy(buf, s.c_str(), size_t(cap) - 1);
+            buf[cap - 1] = 0;
+        }
     });
 }
 
@@ -160,11 +182,16 @@ int orc_solve(orc_system* h, double tol, int max_iter, double* x, mprec_solve_re
         const Op mop = [h](const Vec& v) { return h->prec.apply(v); };
         SolveResult res;
         int attempts = 0, total = 0;
+        std::memset(out, 0, sizeof(*out));
         for (int attempt = 0; attempt < 3; ++attempt) {
             ++attempts;
+            out->attempt_tol[attempt] = opts.tol;
             res = gmres(h->a.dim(), abar, h->sc.b_bar, mop, opts);
             total += res.iterations;
             res.final_true_residual = residual_check(orig, h->b, res.x);
+            out->attempt_iterations[attempt] = res.iterations;
+            out->attempt_converged[attempt] = res.converged;
+            out->attempt_true_residual[attempt] = res.final_true_residual;
             if (!res.converged || res.final_true_residual <= tol) break;
             opts.tol *= 0.5 * tol / res.final_true_residual;
         }
@@ -508,6 +535,7 @@ int orc_gmres(const mprec_bsr* a, const double* b, int prec_kind, void* prec, do
         o.max_iter = max_iter;
         const double t0 = now_s();
         const SolveResult res = gmres(n, aop, Vec(b, b + n), mop, o);
+        std::memset(out, 0, sizeof(*out));
         std::memcpy(x, res.x.data(), res.x.size() * sizeof(double));
         out->iterations = res.iterations;
         out->converged = res.converged;

@@ -101,6 +101,21 @@ def amg_params(strength_threshold=0.25, max_coarse_size=1000, max_levels=25) -> 
     return AmgParams(strength_threshold, max_coarse_size, max_levels)
 
 
+class ScalingOptions(C.Structure):
+    """ScalingOptions (scaling.hpp:22-30): diag_mode 0 = DiagMode::Block, 1 = Scalar."""
+    _fields_ = [("diag_mode", C.c_int), ("second_scaling_from_original", C.c_int)]
+
+
+DIAG_BLOCK, DIAG_SCALAR = 0, 1
+
+
+def scaling_options(diag_mode="block", second_scaling_from_original=False) -> ScalingOptions:
+    modes = {"block": DIAG_BLOCK, "scalar": DIAG_SCALAR, DIAG_BLOCK: DIAG_BLOCK, DIAG_SCALAR: DIAG_SCALAR}
+    if diag_mode not in modes:
+        raise ConfigError(f"unknown diag mode {diag_mode!r}")
+    return ScalingOptions(modes[diag_mode], int(bool(second_scaling_from_original)))
+
+
 class _Bsr(C.Structure):
     _fields_ = [("n_cells", C.c_int), ("nb", C.c_int), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p),
                 ("values", C.c_void_p)]
@@ -113,7 +128,9 @@ class _Csr(C.Structure):
 class _Result(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int), ("attempts", C.c_int),
                 ("history_len", C.c_int), ("final_true_residual", C.c_double), ("setup_s", C.c_double),
-                ("solve_s", C.c_double), ("total_iterations", C.c_int)]
+                ("solve_s", C.c_double), ("total_iterations", C.c_int),
+                ("attempt_iterations", C.c_int * 3), ("attempt_converged", C.c_int * 3),
+                ("attempt_tol", C.c_double * 3), ("attempt_true_residual", C.c_double * 3)]
 
 
 @dataclass
@@ -129,6 +146,10 @@ class SolveResult:
     setup_time_s: float
     wall_time_s: float
     total_iterations: int = 0
+    attempt_iterations: tuple = ()
+    attempt_converged: tuple = ()
+    attempt_tol: tuple = ()
+    attempt_true_residual: tuple = ()
 
 
 def _f64(a) -> np.ndarray:
@@ -263,6 +284,10 @@ class Api:
             "gmres": (C.c_int, [vp, vp, C.c_int, vp, C.c_double, C.c_int, vp, vp, vp, C.c_int]),
         }
         optional = {
+            "setup_opts": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+            "scaling_record": (C.c_int, [vp, C.c_char_p, C.c_int]),
+            "get_levelsets": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, ip, ip]),
+            "amg_get_levelsets": (C.c_int, [vp, C.c_int, C.c_int, ip, ip]),
             "solve_dev": (C.c_int, [vp, C.c_double, C.c_int, vp, vp]),
             "solve_system": (C.c_int, [vp, vp, C.c_int, C.c_double, C.c_int, vp, vp]),
             "device_info": (C.c_int, [ip, ip, ip, i64p]),
@@ -364,7 +389,11 @@ def _result(x, res: _Result, hist) -> SolveResult:
                        breakdown=bool(res.breakdown), attempts=res.attempts,
                        residual_history=np.array(hist[:res.history_len]),
                        final_true_residual=res.final_true_residual, setup_time_s=res.setup_s,
-                       wall_time_s=res.solve_s, total_iterations=res.total_iterations)
+                       wall_time_s=res.solve_s, total_iterations=res.total_iterations,
+                       attempt_iterations=tuple(res.attempt_iterations[:max(res.attempts, 0)]),
+                       attempt_converged=tuple(bool(c) for c in res.attempt_converged[:max(res.attempts, 0)]),
+                       attempt_tol=tuple(res.attempt_tol[:max(res.attempts, 0)]),
+                       attempt_true_residual=tuple(res.attempt_true_residual[:max(res.attempts, 0)]))
 
 
 class System:
@@ -389,7 +418,9 @@ class System:
         except Exception:
             pass
 
-    def setup(self, method, b=None, **amg) -> "System":
+    def setup(self, method, b=None, diag_mode="block", second_scaling_from_original=False, **amg) -> "System":
+        """left_scale(A, b, method, ScalingOptions{diag_mode, second_scaling_from_original})
+        + build_preconditioner(scaled, method, AMGParams{**amg}) (scaling.hpp:65-66, stages.hpp:85-86)."""
         m = parse_method(method) if isinstance(method, str) else int(method)
         if b is None:  # rhs held by the handle (ingested system)
             b = self.b
@@ -397,9 +428,21 @@ class System:
         if self.b.size != self.a.dim:
             raise DimensionError("rhs length mismatch")
         p = amg_params(**amg) if amg else None
-        self.api.call("setup", self.h, m, C.byref(p) if p is not None else None, _ptr(self.b))
+        so = scaling_options(diag_mode, second_scaling_from_original)
+        if self.api.has("setup_opts"):
+            self.api.call("setup_opts", self.h, m, C.byref(p) if p is not None else None, C.byref(so), _ptr(self.b))
+        else:
+            if so.diag_mode != DIAG_BLOCK or so.second_scaling_from_original:
+                raise ConfigError("this implementation has no ScalingOptions entry point")
+            self.api.call("setup", self.h, m, C.byref(p) if p is not None else None, _ptr(self.b))
         self.method = m
         return self
+
+    def scaling_record(self) -> str:
+        """SolveOutcome::scaling_record (harness.cpp:197-201): the applied D factors, in order."""
+        buf = C.create_string_buffer(256)
+        self.api.call("scaling_record", self.h, buf, len(buf))
+        return buf.value.decode()
 
     def write(self, matrix_path: str, layout_path: str, rhs_path: str) -> None:
         """write_block_matrix + write_vector (matrix_io.cpp:93-114); GPU library only."""
@@ -432,13 +475,13 @@ class System:
 
     def scaled(self):
         """(a_bar values, b_bar) of the ScaledSystem (scaling.hpp:36-46)."""
-        av = np.zeros_like(self.a.values)
+        av = np.zeros(self.a.nnzb * self.a.nb * self.a.nb)
         bb = np.zeros(self.a.dim)
         self.api.call("get_scaled", self.h, _ptr(av), _ptr(bb))
         return av, bb
 
     def ilu_values(self) -> np.ndarray:
-        v = np.zeros_like(self.a.values)
+        v = np.zeros(self.a.nnzb * self.a.nb * self.a.nb)
         self.api.call("get_ilu", self.h, _ptr(v))
         return v
 

@@ -4,6 +4,7 @@ with the repo snapshot to the GPU box).
   libmprec_gpu.so  -- the product: sm_100a kernels + C++ host runtime (nvcc)
   libmprec_gen.so  -- synthetic input generator (g++)
   oracle/liboracle.so -- the CPU checker (g++, test infrastructure)
+  oracle/_ref/libmprec_ref.so -- the reference's own sources + Eigen shim (checker pin)
 """
 from __future__ import annotations
 
@@ -41,9 +42,19 @@ def build_gen(force=False):
     return out
 
 
+REFERENCE_SRC = "/root/reference/proj/src"
+
+
 def build_oracle(force=False):
+    """oracle/liboracle.so (the restatement) and, where the reference tree is
+    present (this container; never the GPU box), oracle/_ref/libmprec_ref.so:
+    the reference's own sources compiled against the Eigen-subset shim.
+    Building the checker is not using it: only tests/, smoke() and bench.py's
+    reference arm load these."""
     odir = os.path.join(ROOT, "oracle")
     _run(["make", "-s", "-C", odir] + (["-B"] if force else []))
+    if os.path.isdir(REFERENCE_SRC):
+        _run(["make", "-s", "-C", odir, "ref"] + (["-B"] if force else []))
     return os.path.join(odir, "liboracle.so")
 
 

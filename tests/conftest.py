@@ -29,3 +29,13 @@ def gpu():
     api.call("device_info", C.byref(sm), C.byref(ma), C.byref(mi), C.byref(mem))
     assert (ma.value, mi.value) == (10, 0), f"expected an sm_100 device, got {ma.value}.{mi.value}"
     return api
+
+
+@pytest.fixture(scope="session")
+def ref():
+    """The reference's own sources (oracle/_ref, built against the Eigen-subset
+    shim) through the same ctypes wrapper; skipped where it was not built."""
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref/libmprec_ref.so not built (needs /root/reference at build time)")
+    return oracle.ref_api()

@@ -78,3 +78,18 @@ SMALL_SPECS = {
 
 def small_system(name):
     return gen.generate(gen.make_spec(**SMALL_SPECS[name]))
+
+
+# Members of the config-4 family (reaction band, nb = 8) on which solve_system
+# needs all three tolerance-tightening attempts (harness.cpp:209-217): the
+# scaled residual reaches tol while the true residual does not.
+RETRY_SPECS = {
+    "g20x20_nb8_band_s1": (dict(nx=20, ny=20, nb=8, kappa=1.0, perm_sigma=1.5, band=True, seed=1), "cptr3-amg"),
+    "g60x60_nb8_band_s1": (dict(nx=60, ny=60, nb=8, kappa=1.0, perm_sigma=1.5, band=True, seed=1), "cpr-amg"),
+}
+
+
+def retry_system(name):
+    spec, method = RETRY_SPECS[name]
+    a, b, xs = gen.generate(gen.make_spec(**spec))
+    return a, b, xs, method

@@ -15,7 +15,7 @@ from tests.systems import (laplacian_1d, laplacian_2d, random_block_system, rand
                            small_system)
 
 
-@pytest.fixture(params=["orc", pytest.param("gpu", marks=pytest.mark.gpu)])
+@pytest.fixture(params=["orc", "ref", pytest.param("gpu", marks=pytest.mark.gpu)])
 def api(request):
     return request.getfixturevalue(request.param)
 
