@@ -232,7 +232,14 @@ int mprec_gpu_n_stages(mprec_gpu_system* h, int* n_stages);
 /* stage: index of an AMG stage (CPR: 0; CPTR3: 0 = C_TT, 1 = B_PP). */
 int mprec_gpu_stage_amg(mprec_gpu_system* h, int stage, mprec_gpu_amg** amg);
 
-/* Release (also releases the AMG handles returned by mprec_gpu_stage_amg). */
+/* Level sets of the block-row DAG the ILU(0) factorisation and solves are
+ * scheduled on (ilu0.cpp:16-38, 48-57 on the block pattern):
+ * dir = +1 forward (cell c waits for stored block columns < c), -1 backward;
+ * same convention as mprec_gpu_amg_get_levelsets, one entry per cell. */
+int mprec_gpu_get_levelsets(mprec_gpu_system* h, int dir, int* levels, int* n_levels);
+
+/* Release (also releases the AMG handles returned by mprec_gpu_stage_amg;
+ * a re-setup leaves earlier views stale: they then return MPREC_SETUP). */
 void mprec_gpu_destroy(mprec_gpu_system* h);
 
 /* ---- sub-solver entry points (amg.hpp:21-56, ilu0.hpp:9-24) -------------- */
@@ -249,6 +256,12 @@ int mprec_gpu_amg_get_csr(mprec_gpu_amg* h, int level, int which, int* row_ptr, 
                           double* values);
 /* C/F splitting of level l (1 = C) that produced level l+1 (rs_coarsen). */
 int mprec_gpu_amg_get_cf(mprec_gpu_amg* h, int level, signed char* cf);
+/* Level sets of the symmetric Gauss-Seidel sweep DAG of level l (< n_levels-1):
+ * dir = +1 forward sweep (row i waits for every stored k < i, amg.cpp:31-36),
+ * dir = -1 backward sweep (k > i, amg.cpp:37-42).  levels[i] = 0 for a row
+ * with no dependency, else 1 + max over its dependencies (the Kahn round the
+ * device schedule processes it in); *n_levels = DAG depth.  levels may be NULL. */
+int mprec_gpu_amg_get_levelsets(mprec_gpu_amg* h, int level, int dir, int* levels, int* n_levels);
 void mprec_gpu_amg_destroy(mprec_gpu_amg* h);
 
 /* ILU0Factor::factor / apply (ilu0.cpp:7-59) on a BSR (nb = 1: scalar ILU(0)). */

@@ -7,7 +7,8 @@
 //   reference                                   facade
 //   ---------                                   ------
 //   BlockMatrix::assemble (block_matrix.hpp:56)  BlockMatrix::assemble
-//   parse_method (scaling.hpp:22)               parse_method
+//   MethodSpec / parse_method (scaling.hpp:13-22) MethodSpec / parse_method / method_name
+//   ScalingOptions (scaling.hpp:22-30)          ScalingOptions
 //   left_scale + build_preconditioner           StagePreconditioner::build
 //     (scaling.hpp:65, stages.hpp:85)
 //   StagePreconditioner::apply (stages.hpp:47)  StagePreconditioner::apply
@@ -75,16 +76,61 @@ inline void check(int st) {
     }
 }
 
-// ---- scaling.hpp:10-23 --------------------------------------------------------
-enum class Method { Ilu0 = MPREC_METHOD_ILU0, CprAmg = MPREC_METHOD_CPR_AMG, Cptr3Amg = MPREC_METHOD_CPTR3_AMG };
+// ---- scaling.hpp:10-30 --------------------------------------------------------
+enum class Method { Ilu0, Cpr, Cptr, Cptr3 };
+enum class SubSolver { Direct, Amg };
 
-inline Method parse_method(const std::string& name) {
-    if (name == "ilu0") return Method::Ilu0;
-    if (name == "cpr-amg") return Method::CprAmg;
-    if (name == "cptr3-amg") return Method::Cptr3Amg;
+struct MethodSpec {  // scaling.hpp:13-16
+    Method method = Method::Ilu0;
+    SubSolver sub = SubSolver::Direct;
+};
+
+// parse_method (scaling.cpp:5-15)
+inline MethodSpec parse_method(const std::string& name) {
+    if (name == "ilu0") return {Method::Ilu0, SubSolver::Direct};
+    if (name == "cpr-direct") return {Method::Cpr, SubSolver::Direct};
+    if (name == "cpr-amg") return {Method::Cpr, SubSolver::Amg};
+    if (name == "cptr-direct") return {Method::Cptr, SubSolver::Direct};
     if (name == "cptr-amg") throw ConfigError("cptr supports only the -direct sub-solver");
+    if (name == "cptr3-direct") return {Method::Cptr3, SubSolver::Direct};
+    if (name == "cptr3-amg") return {Method::Cptr3, SubSolver::Amg};
     throw ConfigError("unknown method '" + name + "'");
 }
+
+// method_name (scaling.cpp:17-25)
+inline std::string method_name(const MethodSpec& s) {
+    switch (s.method) {
+        case Method::Ilu0: return "ilu0";
+        case Method::Cpr: return s.sub == SubSolver::Amg ? "cpr-amg" : "cpr-direct";
+        case Method::Cptr: return "cptr-direct";
+        case Method::Cptr3: return s.sub == SubSolver::Amg ? "cptr3-amg" : "cptr3-direct";
+    }
+    return "?";
+}
+
+// MethodSpec -> the C ABI's mprec_method id
+inline int method_id(const MethodSpec& s) {
+    switch (s.method) {
+        case Method::Ilu0: return MPREC_METHOD_ILU0;
+        case Method::Cpr: return s.sub == SubSolver::Amg ? MPREC_METHOD_CPR_AMG : MPREC_METHOD_CPR_DIRECT;
+        case Method::Cptr:
+            if (s.sub == SubSolver::Amg) throw ConfigError("cptr supports only the -direct sub-solver");
+            return MPREC_METHOD_CPTR_DIRECT;
+        case Method::Cptr3: return s.sub == SubSolver::Amg ? MPREC_METHOD_CPTR3_AMG : MPREC_METHOD_CPTR3_DIRECT;
+    }
+    throw ConfigError("unreachable method");
+}
+
+enum class DiagMode { Block, Scalar };  // block_matrix.hpp:46
+
+struct ScalingOptions {  // scaling.hpp:22-30
+    DiagMode diag_mode = DiagMode::Block;
+    bool second_scaling_from_original = false;
+    mprec_scaling_options c() const {
+        return {diag_mode == DiagMode::Scalar ? MPREC_DIAG_SCALAR : MPREC_DIAG_BLOCK,
+                second_scaling_from_original ? 1 : 0};
+    }
+};
 
 struct AMGParams {  // amg.hpp:12-16
     double strength_threshold = 0.25;
@@ -111,6 +157,7 @@ struct SolveResult {  // gmres.hpp:28-36
 struct SolveOutcome {  // harness.hpp:79-83
     SolveResult result;
     double setup_time_s = 0.0;
+    std::string scaling_record;  // applied D factors, ", "-joined (harness.cpp:197-201)
 };
 
 // ---- uniform-layout BlockMatrix (block_matrix.hpp:50-101) --------------------
@@ -157,17 +204,29 @@ struct BlockMatrix {
 // left_scale + build_preconditioner on the device; apply == StagePreconditioner::apply.
 class StagePreconditioner {
    public:
-    static StagePreconditioner build(const BlockMatrix& a, const Vector& b, Method m, const AMGParams& p = {}) {
+    // left_scale(a, b, spec.method, so) + build_preconditioner(scaled, spec, p)
+    static StagePreconditioner build(const BlockMatrix& a, const Vector& b, const MethodSpec& spec,
+                                     const AMGParams& p = {}, const ScalingOptions& so = {}) {
         StagePreconditioner s;
+        const int mid = method_id(spec);
         mprec_gpu_system* h = nullptr;
         const mprec_bsr ca = a.c();
         check(mprec_gpu_create(&ca, &h));
         s.h_.reset(h, mprec_gpu_destroy);
         if (int(b.size()) != a.dim()) throw DimensionError("rhs length mismatch");
         const mprec_amg_params cp = p.c();
-        check(mprec_gpu_setup(h, int(m), &cp, b.data()));
+        const mprec_scaling_options co = so.c();
+        check(mprec_gpu_setup_opts(h, mid, &cp, &co, b.data()));
         s.n_ = a.dim();
+        s.spec_ = spec;
         return s;
+    }
+    MethodSpec spec() const { return spec_; }
+    // ScaledSystem::scaling_record, ", "-joined
+    std::string scaling_record() const {
+        char buf[256];
+        check(mprec_gpu_scaling_record(h_.get(), buf, int(sizeof buf)));
+        return buf;
     }
     int n_stages() const {
         int n = 0;
@@ -206,16 +265,18 @@ class StagePreconditioner {
    private:
     std::shared_ptr<mprec_gpu_system> h_;
     int n_ = 0;
+    MethodSpec spec_;
     mutable double setup_s_ = 0.0;
 };
 
 // solve_system (harness.hpp:87-88, harness.cpp:190-219)
-inline SolveOutcome solve_system(const BlockMatrix& a, const Vector& b, Method m, double tol = 1e-8,
+inline SolveOutcome solve_system(const BlockMatrix& a, const Vector& b, const MethodSpec& method, double tol = 1e-8,
                                  int max_iter = 500) {
-    const StagePreconditioner p = StagePreconditioner::build(a, b, m);
+    const StagePreconditioner p = StagePreconditioner::build(a, b, method);
     SolveOutcome out;
     out.result = p.solve(tol, max_iter);
     out.setup_time_s = p.setup_time_s();
+    out.scaling_record = p.scaling_record();
     return out;
 }
 

@@ -1070,6 +1070,18 @@ SolveOutcome solve_system(const Bsr& a, const Vec& b, Method m, double tol, int 
     return out;
 }
 
+// Backward sweep (amg.cpp:37-42, ilu0.cpp:52-57): row i waits for stored k > i.
+std::vector<int> level_sets_upper(const Csr& a) {
+    std::vector<int> lev(a.rows, 0);
+    for (int i = a.rows - 1; i >= 0; --i) {
+        int l = 0;
+        for (int k = a.rp[i]; k < a.rp[i + 1]; ++k)
+            if (a.ci[k] > i) l = std::max(l, lev[a.ci[k]] + 1);
+        lev[i] = l;
+    }
+    return lev;
+}
+
 std::vector<int> level_sets_lower(const Csr& a) {
     std::vector<int> lev(a.rows, 0);
     for (int i = 0; i < a.rows; ++i) {

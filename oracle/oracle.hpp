@@ -236,6 +236,7 @@ SolveOutcome solve_system(const Bsr& a, const Vec& b, Method m, double tol = 1e-
 // stored k < i in row i); the reference has none, these are the schedule the
 // GPU sweeps must honour.
 std::vector<int> level_sets_lower(const Csr& a);
+std::vector<int> level_sets_upper(const Csr& a);  // backward sweep: row i depends on stored k > i
 
 // ----- static condensation (proj/src/condense.cpp:206-258) ------------------
 // GlobalJacobian (condense.hpp:64-81) with uniform np x np primary blocks;

@@ -487,6 +487,35 @@ int orc_amg_get_cf(orc_amg* hh, int level, signed char* cf) {
     });
 }
 
+static void levels_out(const std::vector<int>& l, int* levels, int* n_levels) {
+    int nl = 0;
+    for (int v : l) nl = std::max(nl, v + 1);
+    if (levels) std::memcpy(levels, l.data(), l.size() * sizeof(int));
+    if (n_levels) *n_levels = nl;
+}
+
+int orc_amg_get_levelsets(orc_amg* hh, int level, int dir, int* levels, int* n_levels) {
+    return guard([&] {
+        auto* h = reinterpret_cast<AMGHierarchy*>(hh);
+        if (level < 0 || level + 1 >= h->n_levels()) throw Error(INDEX, "level is not smoothed");
+        if (dir != 1 && dir != -1) throw Error(INDEX, "dir must be +1 or -1");
+        const Csr& a = h->levels[level].a;
+        levels_out(dir > 0 ? level_sets_lower(a) : level_sets_upper(a), levels, n_levels);
+    });
+}
+
+int orc_get_levelsets(orc_system* h, int dir, int* levels, int* n_levels) {
+    return guard([&] {
+        if (dir != 1 && dir != -1) throw Error(INDEX, "dir must be +1 or -1");
+        Csr p;  // the block pattern as a cell-level CSR
+        p.rows = p.cols = h->a.nc;
+        p.rp = h->a.rp;
+        p.ci = h->a.ci;
+        p.v.assign(p.ci.size(), 1.0);
+        levels_out(dir > 0 ? level_sets_lower(p) : level_sets_upper(p), levels, n_levels);
+    });
+}
+
 void orc_amg_destroy(orc_amg* hh) { delete reinterpret_cast<AMGHierarchy*>(hh); }
 
 int orc_ilu_create(const mprec_bsr* a, orc_ilu** out) {

@@ -286,8 +286,8 @@ class Api:
         optional = {
             "setup_opts": (C.c_int, [vp, C.c_int, vp, vp, vp]),
             "scaling_record": (C.c_int, [vp, C.c_char_p, C.c_int]),
-            "get_levelsets": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, ip, ip]),
-            "amg_get_levelsets": (C.c_int, [vp, C.c_int, C.c_int, ip, ip]),
+            "get_levelsets": (C.c_int, [vp, C.c_int, vp, ip]),
+            "amg_get_levelsets": (C.c_int, [vp, C.c_int, C.c_int, vp, ip]),
             "solve_dev": (C.c_int, [vp, C.c_double, C.c_int, vp, vp]),
             "solve_system": (C.c_int, [vp, vp, C.c_int, C.c_double, C.c_int, vp, vp]),
             "device_info": (C.c_int, [ip, ip, ip, i64p]),
@@ -485,6 +485,14 @@ class System:
         self.api.call("get_ilu", self.h, _ptr(v))
         return v
 
+    def levelsets(self, direction: int = 1):
+        """(levels per cell, depth) of the block-row DAG the ILU(0) sweeps are
+        scheduled on; direction +1 forward, -1 backward."""
+        out = np.zeros(self.a.n_cells, np.int32)
+        nl = C.c_int()
+        self.api.call("get_levelsets", self.h, int(direction), _ptr(out), C.byref(nl))
+        return out, nl.value
+
     def n_stages(self) -> int:
         n = C.c_int()
         self.api.call("n_stages", self.h, C.byref(n))
@@ -549,6 +557,14 @@ class AMGHierarchy:
         out = np.zeros(n, np.int8)
         self.api.call("amg_get_cf", self.h, l, _ptr(out))
         return out
+
+    def levelsets(self, l: int, direction: int = 1):
+        """(levels per row, depth) of level l's Gauss-Seidel sweep DAG."""
+        n, _, _ = self.level_info(l)
+        out = np.zeros(n, np.int32)
+        nl = C.c_int()
+        self.api.call("amg_get_levelsets", self.h, l, int(direction), _ptr(out), C.byref(nl))
+        return out, nl.value
 
     def apply(self, r) -> np.ndarray:
         r = _f64(r)

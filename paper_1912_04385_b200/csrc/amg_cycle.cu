@@ -408,15 +408,33 @@ namespace mg {
 // row-per-warp (cross-SM hops), CTA bands of 4096 / 8192 rows (on-SM hops) or
 // band-segment chains (gs_seg.cu) or a whole level in one thread block cluster
 // (gs_cluster.cu).  MPREC_GS_MODE forces one: warp | cta | seg | cluster.
+// LS group counts by level size, in order of preference (B200 measurements,
+// DESIGN.md §5.1); the next one is tried when a program does not fit.
+static std::vector<int> ls_group_counts(int n) {
+    if (n >= (1 << 20)) return {74, 148, 37};
+    if (n >= 300000) return {148, 74, 37};
+    if (n >= 50000) return {74, 148, 37};
+    if (n >= 8192) return {37, 16, 8, 4};
+    return {16, 8, 4, 2, 1};  // small levels: one warp may beat any pipeline
+}
+
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     L.cta_B = 0;
     L.seg = false;
     L.ls_fwd = LsSched();
     L.ls_bwd = LsSched();
-    const std::string force = [] {  // read per setup so tests can force each kernel
+    std::string force = [] {  // read per setup so tests can force each kernel
         const char* e = getenv("MPREC_GS_MODE");
         return std::string(e ? e : "");
     }();
+    // The sweep kernels round a row's sum in different orders (the LS program
+    // pre-scales by 1/a_ii and sums the previous iterate's part first), so the
+    // kernel choice must not depend on timing: the default is a fixed rule (the
+    // first LS program that fits, the cluster kernel on levels whose iterate fits
+    // one cluster, else the warp-per-row sweep) and setups are bitwise
+    // reproducible.  MPREC_GS_MODE=tune restores the timed search (experiments).
+    const bool timed = force == "tune";
+    if (timed) force.clear();
     L.cl_size = 0;
     if (force == "warp") return;
     if (force == "ls") {
@@ -449,6 +467,24 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         return;
     }
     const bool try_ls = L.glev_f && L.glev_b && L.n >= 512;
+    if (force.empty() && !timed) {
+        if (try_ls && csr_sorted(c, L.a))
+            for (int K : ls_group_counts(L.n))
+                if (build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) {
+                    if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: level-sync K=%d\n", L.n, K);
+                    return;
+                }
+        if (cl_size > 0) {
+            L.cl_size = cl_size;
+            L.cl_R = cl_R;
+            build_band_order(c, L.n, sf.level.p, cl_R, L.border_f);
+            build_band_order(c, L.n, sb.level.p, cl_R, L.border_b);
+            if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: cluster of %d\n", L.n, cl_size);
+            return;
+        }
+        if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: row-per-warp\n", L.n);
+        return;
+    }
     // million-row levels: the level-synchronous program beats the band kernels by
     // 3-4x, so their schedules are not built and timed
     if (force.empty() && !try_cta && !try_seg && !try_cl && !try_ls) return;
@@ -494,17 +530,7 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
     LsSched ls_bf, ls_bb;
     float t_ls = 1e30f;
     if (try_ls && sorted && force.empty()) {
-        std::vector<int> cands;
-        if (L.n >= (1 << 20))
-            cands = {74, 148, 37};
-        else if (L.n >= 300000)
-            cands = {148, 74, 37};
-        else if (L.n >= 50000)
-            cands = {74, 148, 37};
-        else if (L.n >= 8192)
-            cands = {37, 16, 8, 4};
-        else
-            cands = {16, 8, 4, 2, 1};  // small levels: one warp may beat any pipeline
+        const std::vector<int> cands = ls_group_counts(L.n);
         const bool first_fit = L.n >= 50000;  // large levels: the first program that fits
         for (int K : cands) {
             if (!build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) continue;

@@ -124,6 +124,10 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
     if (tol <= 0.0) throw Error(MPREC_DIMENSION, "gmres: tolerance must be positive");
     GmresOut out;
     double* sc = c.scal.p;  // [0] bnorm [1] pre_norm [2] wn [3] norm after reorth
+    // work vectors first: the caller's true-residual check uses kr.t even when
+    // b = 0 returns early (gmres.cpp:17-21)
+    kr.w.ensure(n);
+    kr.t.ensure(n);
     nrm2(c, b, n, sc + 0);
     double bnorm = 0.0;
     MG_CUDA(cudaMemcpyAsync(&bnorm, sc + 0, sizeof(double), cudaMemcpyDeviceToHost, c.s));
@@ -136,8 +140,6 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
     }
     const int max_it = int(std::min<int64_t>(max_iter, n));
     kr.V.n = n;
-    kr.w.ensure(n);
-    kr.t.ensure(n);
     kr.hcol.ensure(max_it + 2);
     kr.vk.ensure(n);
     kr.ct.ensure(max_it / kBasisChunk + 2);
@@ -240,6 +242,12 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
 void fill_result(mprec_solve_result* r, const GmresOut& g, int attempts, double setup_s, double solve_s,
                  double* history, int cap, int total_iterations = -1) {
     if (!r) return;
+    for (int q = 0; q < 3; ++q) {
+        r->attempt_iterations[q] = q == 0 ? g.iterations : 0;
+        r->attempt_converged[q] = q == 0 ? g.converged : 0;
+        r->attempt_tol[q] = 0.0;
+        r->attempt_true_residual[q] = q == 0 ? g.final_true_residual : 0.0;
+    }
     r->total_iterations = total_iterations < 0 ? g.iterations : total_iterations;
     r->iterations = g.iterations;
     r->converged = g.converged;
@@ -258,6 +266,19 @@ void fill_result(mprec_solve_result* r, const GmresOut& g, int attempts, double 
 }  // namespace
 
 static bool is_cptr3_method(int m) { return m == MPREC_METHOD_CPTR3_AMG || m == MPREC_METHOD_CPTR3_DIRECT; }
+
+// ScaledSystem::scaling_record (scaling.cpp:84, 102, 116, 144) joined as in
+// solve_system (harness.cpp:197-201)
+static std::string scaling_record_of(int m) {
+    switch (m) {
+        case MPREC_METHOD_CPR_AMG:
+        case MPREC_METHOD_CPR_DIRECT: return "D_Ph*D_hh^-1";
+        case MPREC_METHOD_CPTR_DIRECT: return "D_es*D_ss^-1";
+        case MPREC_METHOD_CPTR3_AMG:
+        case MPREC_METHOD_CPTR3_DIRECT: return "[D_Ps;D_Ts]*D_ss^-1, D_Tp*D_PP^-1";
+        default: return "";
+    }
+}
 
 namespace mg {
 void ingest(Ctx& c, const char* mtx, const char* layout, const char* rhs, Pattern& pat, DBuf<double>& val, int* n_cells,
@@ -314,6 +335,7 @@ struct mprec_gpu_system {
     Krylov kr;
     std::vector<std::unique_ptr<mprec_gpu_amg>> views;
     std::vector<double> b_host;  // rhs kept by mprec_gpu_ingest / the last setup
+    std::string scaling_record;
 
     BsrView A() { return view_of(pat, nb, a_val.p); }
     BsrView Abar() { return view_of(pat, nb, abar_val.p); }
@@ -390,6 +412,17 @@ struct mprec_gpu_system {
     }
 
     int total_iterations = 0;
+    int att_it[3] = {0, 0, 0}, att_cv[3] = {0, 0, 0};
+    double att_tol[3] = {0, 0, 0}, att_res[3] = {0, 0, 0};
+    void log_attempts(mprec_solve_result* r) const {
+        if (!r) return;
+        for (int q = 0; q < 3; ++q) {
+            r->attempt_iterations[q] = att_it[q];
+            r->attempt_converged[q] = att_cv[q];
+            r->attempt_tol[q] = att_tol[q];
+            r->attempt_true_residual[q] = att_res[q];
+        }
+    }
     GmresOut solve_attempts(double tol, int max_iter, double* xdev, int* attempts) {
         Ctx& c = ctx;
         // MPREC_PROFILE_SOLVE=1: bracket the solve for `ncu --profile-from-start off`
@@ -416,10 +449,17 @@ struct mprec_gpu_system {
         GmresOut res;
         *attempts = 0;
         total_iterations = 0;
+        for (int q = 0; q < 3; ++q) {
+            att_it[q] = att_cv[q] = 0;
+            att_tol[q] = att_res[q] = 0.0;
+        }
         for (int attempt = 0; attempt < 3; ++attempt) {
             ++*attempts;
+            att_tol[attempt] = opt_tol;
             res = gmres_dev(c, kr, n, Aop, Mop, bbar.p, opt_tol, max_iter, xdev);
             total_iterations += res.iterations;
+            att_it[attempt] = res.iterations;
+            att_cv[attempt] = res.converged;
             // residual_check on the ORIGINAL system (gmres.cpp:108-112)
             bsr_spmv(c, A(), xdev, kr.t.p, bn == 0.0 ? nullptr : b.p, MPREC_K_SPMV);
             nrm2(c, kr.t.p, n, c.scal.p + 9);
@@ -427,6 +467,7 @@ struct mprec_gpu_system {
             MG_CUDA(cudaMemcpyAsync(&rn, c.scal.p + 9, sizeof(double), cudaMemcpyDeviceToHost, c.s));
             c.sync();
             res.final_true_residual = bn == 0.0 ? rn : rn / bn;
+            att_res[attempt] = res.final_true_residual;
             if (!res.converged || res.final_true_residual <= tol) break;
             opt_tol *= 0.5 * tol / res.final_true_residual;
         }
@@ -469,6 +510,11 @@ int mprec_gpu_create(const mprec_bsr* a, mprec_gpu_system** out) {
 }
 
 int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg, const double* b) {
+    return mprec_gpu_setup_opts(h, method, amg, nullptr, b);
+}
+
+int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params* amg,
+                         const mprec_scaling_options* opts, const double* b) {
     return guard([&] {
         if (!h) throw Error(MPREC_DIMENSION, "null handle");
         if (method < MPREC_METHOD_ILU0 || method > MPREC_METHOD_CPTR3_DIRECT)
@@ -494,7 +540,12 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
         // left_scale (scaling.cpp:149-158)
         {
             Trace tr(&c, "left_scale");
-            left_scale(c, h->Abar(), h->bbar.p, method);
+            const int scalar_diag = opts && opts->diag_mode == MPREC_DIAG_SCALAR;
+            if (opts && opts->diag_mode != MPREC_DIAG_BLOCK && opts->diag_mode != MPREC_DIAG_SCALAR)
+                throw Error(MPREC_CONFIG, "unknown diag mode " + std::to_string(opts->diag_mode));
+            const bool from_orig = opts && opts->second_scaling_from_original;
+            left_scale(c, h->Abar(), h->bbar.p, method, scalar_diag, from_orig ? h->a_val.p : nullptr);
+            h->scaling_record = scaling_record_of(method);
         }
         // build_preconditioner (stages.cpp:129-138)
         AmgParams prm;
@@ -504,7 +555,9 @@ int mprec_gpu_setup(mprec_gpu_system* h, int method, const mprec_amg_params* amg
             prm.max_levels = amg->max_levels;
         }
         const int nc = h->pat.nc;
-        h->views.clear();
+        // views handed out by mprec_gpu_stage_amg go stale (not freed: a caller may
+        // still hold them; every AMG entry point rejects a stale view)
+        for (auto& v : h->views) v->amg = nullptr;
         h->amgT.reset();
         h->amgP.reset();
         h->amgE.reset();
@@ -760,6 +813,7 @@ int mprec_gpu_solve_dev(mprec_gpu_system* h, double tol, int max_iter, double* x
         const GmresOut g = h->solve_attempts(tol, max_iter, xd, &attempts);
         h->ctx.sync();
         fill_result(out, g, attempts, h->setup_s, now_s() - t0, nullptr, 0, h->total_iterations);
+        h->log_attempts(out);
     });
 }
 
@@ -773,6 +827,7 @@ int mprec_gpu_solve(mprec_gpu_system* h, double tol, int max_iter, double* x, mp
         h->x.download(x, h->n, h->ctx.s);
         h->ctx.sync();
         fill_result(out, g, attempts, h->setup_s, now_s() - t0, history, history_cap, h->total_iterations);
+        h->log_attempts(out);
     });
 }
 
@@ -790,6 +845,15 @@ int mprec_gpu_solve_system(const mprec_bsr* a, const double* b, int method, doub
         g_payload = kp;
     }
     return st;
+}
+
+int mprec_gpu_scaling_record(mprec_gpu_system* h, char* buf, int cap) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        if (!buf || cap < 1) throw Error(MPREC_DIMENSION, "empty buffer");
+        std::strncpy(buf, h->scaling_record.c_str(), size_t(cap) - 1);
+        buf[cap - 1] = 0;
+    });
 }
 
 int mprec_gpu_get_scaled(mprec_gpu_system* h, double* abar, double* bbar) {
@@ -824,6 +888,11 @@ int mprec_gpu_stage_amg(mprec_gpu_system* h, int stage, mprec_gpu_amg** out) {
         if (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) a = h->amgT.get();
         if (h->method == MPREC_METHOD_CPTR3_AMG && stage == 1) a = h->amgP.get();
         if (!a) throw Error(MPREC_INDEX, "not an AMG stage");
+        for (auto& v : h->views)  // one live view per stage hierarchy
+            if (v->amg == a) {
+                *out = v.get();
+                return;
+            }
         auto v = std::make_unique<mprec_gpu_amg>();
         v->ctx = &h->ctx;
         v->amg = a;
@@ -881,6 +950,7 @@ int mprec_gpu_amg_create(const mprec_csr* a, const mprec_amg_params* p, mprec_gp
 
 int mprec_gpu_amg_apply(mprec_gpu_amg* h, const double* r, double* x) {
     return guard([&] {
+        if (!h || !h->amg) throw Error(MPREC_SETUP, "stale AMG view: its system was set up again");
         Ctx& c = *h->ctx;
         const int n = h->amg->lv[0]->n;
         h->r.upload(r, std::max(n, 1), c.s);
@@ -892,11 +962,15 @@ int mprec_gpu_amg_apply(mprec_gpu_amg* h, const double* r, double* x) {
 }
 
 int mprec_gpu_amg_n_levels(mprec_gpu_amg* h, int* n) {
-    return guard([&] { *n = h->amg->n_levels(); });
+    return guard([&] {
+        if (!h || !h->amg) throw Error(MPREC_SETUP, "stale AMG view: its system was set up again");
+        *n = h->amg->n_levels();
+    });
 }
 
 int mprec_gpu_amg_level_info(mprec_gpu_amg* h, int l, int* n, int* nnz_a, int* nnz_p) {
     return guard([&] {
+        if (!h || !h->amg) throw Error(MPREC_SETUP, "stale AMG view: its system was set up again");
         if (l < 0 || l >= h->amg->n_levels()) throw Error(MPREC_INDEX, "level out of range");
         const AmgLevel& L = *h->amg->lv[l];
         *n = L.n;
@@ -907,6 +981,7 @@ int mprec_gpu_amg_level_info(mprec_gpu_amg* h, int l, int* n, int* nnz_a, int* n
 
 int mprec_gpu_amg_get_csr(mprec_gpu_amg* h, int l, int which, int* rp, int* ci, double* v) {
     return guard([&] {
+        if (!h || !h->amg) throw Error(MPREC_SETUP, "stale AMG view: its system was set up again");
         if (l < 0 || l >= h->amg->n_levels()) throw Error(MPREC_INDEX, "level out of range");
         if (which != 0 && l == 0) throw Error(MPREC_INDEX, "level 0 has no P/R");
         Ctx& c = *h->ctx;
@@ -919,8 +994,47 @@ int mprec_gpu_amg_get_csr(mprec_gpu_amg* h, int l, int which, int* rp, int* ci, 
     });
 }
 
+static void levels_out(Ctx& c, const int* dev_levels, int n, int nlev, int* levels, int* n_levels) {
+    if (levels && n > 0) MG_CUDA(cudaMemcpyAsync(levels, dev_levels, sizeof(int) * n, cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    if (n_levels) *n_levels = nlev;
+}
+
+int mprec_gpu_amg_get_levelsets(mprec_gpu_amg* h, int l, int dir, int* levels, int* n_levels) {
+    return guard([&] {
+        if (!h || !h->amg) throw Error(MPREC_SETUP, "stale AMG view: its system was set up again");
+        if (l < 0 || l + 1 >= h->amg->n_levels()) throw Error(MPREC_INDEX, "level is not smoothed");
+        if (dir != 1 && dir != -1) throw Error(MPREC_INDEX, "dir must be +1 or -1");
+        const AmgLevel& L = *h->amg->lv[l];
+        const int* lev = dir > 0 ? L.glev_f : L.glev_b;
+        if (!lev) throw Error(MPREC_SETUP, "no sweep schedule on this level");
+        // level 0 may borrow the block pattern's schedule (same DAG, shared)
+        const Sched& own = dir > 0 ? L.own_fwd : L.own_bwd;
+        int nlev = own.nlev;
+        if (lev != own.level.p) {
+            std::vector<int> hl(L.n);
+            MG_CUDA(cudaMemcpyAsync(hl.data(), lev, sizeof(int) * L.n, cudaMemcpyDeviceToHost, h->ctx->s));
+            h->ctx->sync();
+            nlev = 0;
+            for (int v : hl) nlev = std::max(nlev, v + 1);
+        }
+        levels_out(*h->ctx, lev, L.n, nlev, levels, n_levels);
+    });
+}
+
+int mprec_gpu_get_levelsets(mprec_gpu_system* h, int dir, int* levels, int* n_levels) {
+    return guard([&] {
+        if (!h) throw Error(MPREC_DIMENSION, "null handle");
+        if (dir != 1 && dir != -1) throw Error(MPREC_INDEX, "dir must be +1 or -1");
+        h->pat.ensure_sched(h->ctx);
+        const Sched& s = dir > 0 ? h->pat.fwd : h->pat.bwd;
+        levels_out(h->ctx, s.level.p, h->pat.nc, s.nlev, levels, n_levels);
+    });
+}
+
 int mprec_gpu_amg_get_cf(mprec_gpu_amg* h, int l, signed char* cf) {
     return guard([&] {
+        if (!h || !h->amg) throw Error(MPREC_SETUP, "stale AMG view: its system was set up again");
         if (l < 0 || l + 1 >= h->amg->n_levels()) throw Error(MPREC_INDEX, "level has no coarsening");
         Ctx& c = *h->ctx;
         const AmgLevel& L = *h->amg->lv[l];
@@ -1005,6 +1119,8 @@ int mprec_gpu_gmres(const mprec_bsr* a, const double* b, int prec_kind, void* pr
             Mop = [&, ah](const double* xx, double* yy) { ah->amg->apply(*c, xx, yy); };
         } else {
             auto* ih = static_cast<mprec_gpu_ilu*>(prec);
+            if (int64_t(ih->ilu.lu.nc) * ih->ilu.lu.nb != n)
+                throw Error(MPREC_DIMENSION, "preconditioner dimension mismatch");
             Mop = [&, ih](const double* xx, double* yy) { ih->ilu.apply(*c, xx, yy); };
         }
         const double t0 = now_s();

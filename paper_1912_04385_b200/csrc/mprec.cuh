@@ -125,7 +125,10 @@ void bsr_col_update(Ctx& c, const BsrView& a, int f, const double* xs, const dou
 // ---- scaling.cu --------------------------------------------------------------
 // In-place left scaling of Ā and b̄ (scaling.cpp:73-147); throws mg::Error
 // (SINGULAR_BLOCK with the reference's tag and cell) after synchronising.
-void left_scale(Ctx& c, const BsrView& abar, double* bbar, int method);
+// scalar_diag: ScalingOptions::diag_mode == Scalar; orig_for_pp: the original
+// A's values when second_scaling_from_original (else nullptr)
+void left_scale(Ctx& c, const BsrView& abar, double* bbar, int method, int scalar_diag = 0,
+                const double* orig_for_pp = nullptr);
 // vals[k] = A_k(f, f)  (extract_submatrix on a single field, pattern = block pattern)
 void extract_field(Ctx& c, const BsrView& a, int f, double* vals);
 // B_ee (CPTR): CSR with 2 n_c rows, cell-interleaved (P, T); erp[2nc+1], eci/ev[4 nnzb]

@@ -105,8 +105,11 @@ __device__ void scaling_w(const double* d, int nb, const int* tl, int nt, const 
         }
 }
 
-// CPR (scaling.cpp:73-88): P rows -= (D_Ph D_hh^-1) * h rows, h = s..., T
-__global__ void k_scale_cpr(const int* rp, const int* dpos, double* val, double* b, int nc, int nb, int* err) {
+// CPR (scaling.cpp:73-88): P rows -= (D_Ph D_hh^-1) * h rows, h = s..., T.
+// scalar_diag: DiagMode::Scalar -- D_hh is the diagonal of the cell block
+// (block_diagonal_of, block_matrix.cpp:186-193); D_Ph stays the full block.
+__global__ void k_scale_cpr(const int* rp, const int* dpos, double* val, double* b, int nc, int nb, int* err,
+                            int scalar_diag) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nc) return;
     const int ns = nb - 2, P = nb - 2, T = nb - 1, m = ns + 1;
@@ -116,7 +119,7 @@ __global__ void k_scale_cpr(const int* rp, const int* dpos, double* val, double*
     double dss[kMaxNb * kMaxNb], lu[kMaxNb * kMaxNb], inv[kMaxNb * kMaxNb], w[kMaxNb];
     const double* d = val + (int64_t)dpos[c] * nb * nb;
     for (int j = 0; j < m; ++j)
-        for (int i = 0; i < m; ++i) dss[j * m + i] = d[sl[j] * nb + sl[i]];
+        for (int i = 0; i < m; ++i) dss[j * m + i] = (scalar_diag && i != j) ? 0.0 : d[sl[j] * nb + sl[i]];
     if (!invert_small(dss, m, inv, lu, perm)) {
         atomicMin(err + 0, c);
         return;
@@ -126,9 +129,11 @@ __global__ void k_scale_cpr(const int* rp, const int* dpos, double* val, double*
 }
 
 // CPTR3 (scaling.cpp:107-147): e = {P,T} rows -= (D_es D_ss^-1) * s rows, then
-// T rows -= (D_Tp * (1/D_PP)) * P rows on the once-scaled block row.
+// T rows -= (D_Tp * (1/D_PP)) * P rows on the once-scaled block row; D_PP of
+// the once-scaled row or, with second_scaling_from_original (scaling.cpp:126),
+// of the original A (orig).
 __global__ void k_scale_cptr3(const int* rp, const int* dpos, double* val, double* b, int nc, int nb, int* err,
-                              int second) {
+                              int second, int scalar_diag, const double* orig) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nc) return;
     const int ns = nb - 2, P = nb - 2, T = nb - 1;
@@ -138,7 +143,7 @@ __global__ void k_scale_cptr3(const int* rp, const int* dpos, double* val, doubl
         for (int k = 0; k < ns; ++k) sl[k] = k;
         double dss[kMaxNb * kMaxNb], lu[kMaxNb * kMaxNb], inv[kMaxNb * kMaxNb], w[2 * kMaxNb];
         for (int j = 0; j < ns; ++j)
-            for (int i = 0; i < ns; ++i) dss[j * ns + i] = d[sl[j] * nb + sl[i]];
+            for (int i = 0; i < ns; ++i) dss[j * ns + i] = (scalar_diag && i != j) ? 0.0 : d[sl[j] * nb + sl[i]];
         if (!invert_small(dss, ns, inv, lu, perm)) {
             atomicMin(err + 0, c);
             return;
@@ -147,7 +152,7 @@ __global__ void k_scale_cptr3(const int* rp, const int* dpos, double* val, doubl
         combine_cell(rp, val, b, c, nb, tl, 2, sl, ns, w);
     }
     if (!second) return;  // CPTR (scaling.cpp:90-105): first scaling only
-    const double pp = d[P * nb + P];
+    const double pp = orig ? orig[(int64_t)dpos[c] * nb * nb + P * nb + P] : d[P * nb + P];
     // inverted_copy of the 1x1 block: tol = 1e-12|pp| -> fails iff |pp| <= tol
     if (fabs(pp) <= 1e-12 * fabs(pp)) {
         atomicMin(err + 1, c);
@@ -190,7 +195,7 @@ void extract_pt(Ctx& c, const BsrView& a, int* erp, int* eci, double* ev) {
     check_launch("extract_pt");
 }
 
-void left_scale(Ctx& c, const BsrView& a, double* bbar, int method) {
+void left_scale(Ctx& c, const BsrView& a, double* bbar, int method, int scalar_diag, const double* orig_for_pp) {
     if (method == MPREC_METHOD_ILU0) return;
     if (a.nb < 2) throw Error(MPREC_DIMENSION, "CPR/CPTR3 need P and T unknowns (nb >= 2)");
     if (a.nb > kMaxNb) throw Error(MPREC_DIMENSION, "nb > 16 not supported by the scaling kernel");
@@ -201,11 +206,11 @@ void left_scale(Ctx& c, const BsrView& a, double* bbar, int method) {
         Ctx::Scope sc(&c, MPREC_K_BLAS1, 2.0 * a.nnzb * 8.0 * a.nb * a.nb);
         const int th = 128, g = (a.nc + th - 1) / th;
         if (method == MPREC_METHOD_CPR_AMG || method == MPREC_METHOD_CPR_DIRECT)
-            k_scale_cpr<<<g, th, 0, c.s>>>(a.rp, a.dpos, a.val, bbar, a.nc, a.nb, c.err.p);
+            k_scale_cpr<<<g, th, 0, c.s>>>(a.rp, a.dpos, a.val, bbar, a.nc, a.nb, c.err.p, scalar_diag);
         else if (method == MPREC_METHOD_CPTR3_AMG || method == MPREC_METHOD_CPTR3_DIRECT ||
                  method == MPREC_METHOD_CPTR_DIRECT)
             k_scale_cptr3<<<g, th, 0, c.s>>>(a.rp, a.dpos, a.val, bbar, a.nc, a.nb, c.err.p,
-                                             method != MPREC_METHOD_CPTR_DIRECT);
+                                             method != MPREC_METHOD_CPTR_DIRECT, scalar_diag, orig_for_pp);
         else
             throw Error(MPREC_CONFIG, "unknown method id " + std::to_string(method));
         check_launch("left_scale");

@@ -22,6 +22,10 @@ def orc():
 @pytest.fixture(scope="session")
 def gpu():
     """The B200 library.  Fails loudly (no fallback) when it cannot run."""
+    if os.environ.get("MPREC_TEST_GPU_AS") == "ref":
+        # development aid: run the -m gpu tests' logic against the reference build
+        import oracle
+        return oracle.ref_api()
     from paper_1912_04385_b200.api import gpu as _gpu
     api = _gpu()
     import ctypes as C

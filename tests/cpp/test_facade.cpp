@@ -121,6 +121,38 @@ int main() {
                         o.result.final_true_residual);
         }
     }
+    // MethodSpec{Method, SubSolver} incl. the -direct sub-solvers, ScalingOptions,
+    // scaling_record (scaling.hpp:13-30, harness.hpp:79-83)
+    {
+        mprec_gen_spec s{12, 10, 4, 1.0, 1.0, 1, 7};
+        BlockMatrix a;
+        a.n_cells = s.nx * s.ny;
+        a.nb = s.nb;
+        const int64_t nnzb = mprec_gen_nnzb(s.nx, s.ny);
+        a.row_ptr.resize(a.n_cells + 1);
+        a.col_idx.resize(nnzb);
+        a.values.resize(size_t(nnzb) * s.nb * s.nb);
+        Vector xs(a.dim()), b(a.dim());
+        mprec_gen_pattern(s.nx, s.ny, a.row_ptr.data(), a.col_idx.data());
+        mprec_gen_fill(&s, a.row_ptr.data(), a.col_idx.data(), a.values.data(), xs.data(), b.data(), 1);
+        for (const char* name : {"ilu0", "cpr-direct", "cpr-amg", "cptr-direct", "cptr3-direct", "cptr3-amg"}) {
+            const MethodSpec spec = parse_method(name);
+            CHECK(method_name(spec) == name);
+            const SolveOutcome o = solve_system(a, b, spec);
+            CHECK(o.result.converged && o.result.final_true_residual <= 1e-8);
+            std::printf("ok %s: %d iterations, scaling record '%s'\n", name, o.result.iterations,
+                        o.scaling_record.c_str());
+        }
+        CHECK(solve_system(a, b, parse_method("cptr3-amg")).scaling_record == "[D_Ps;D_Ts]*D_ss^-1, D_Tp*D_PP^-1");
+        CHECK(solve_system(a, b, parse_method("cpr-amg")).scaling_record == "D_Ph*D_hh^-1");
+        ScalingOptions so;
+        so.diag_mode = DiagMode::Scalar;
+        so.second_scaling_from_original = true;
+        const StagePreconditioner p = StagePreconditioner::build(a, b, {Method::Cptr3, SubSolver::Amg}, {}, so);
+        const SolveResult r = p.solve();
+        CHECK(r.converged && p.n_stages() == 3 && p.spec().sub == SubSolver::Amg);
+        std::printf("ok ScalingOptions{Scalar, from original}: %d iterations\n", r.iterations);
+    }
     // BlockMatrix::assemble semantics: duplicates summed, zero diagonal inserted
     {
         const BlockMatrix m = BlockMatrix::assemble(2, 1, {{{0, 1}, {1.0}}, {{0, 1}, {2.0}}, {{1, 1}, {5.0}}});
