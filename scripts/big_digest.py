@@ -1,7 +1,7 @@
 """Setup digests + solve record of one BASELINE config on one implementation.
 
     python scripts/big_digest.py IMPL CID [--iters K] [--out PATH] [--method M]
-                                 [--apply-sample] [--perturb EPS] [--no-setup-digest]
+                                 [--apply-sample] [--perturb-seed S] [--no-setup-digest]
 
 IMPL = gpu | oracle | ref.  Writes the record of tests/bigcase.py as .npz.
 """
@@ -34,10 +34,10 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-setup-digest", action="store_true")
     ap.add_argument("--apply-sample", action="store_true")
-    ap.add_argument("--perturb", type=float, default=0.0)
+    ap.add_argument("--perturb-seed", type=int, default=None)
     args = ap.parse_args()
     blob = run_case(bind(args.impl), args.cid, args.iters, args.method, not args.no_setup_digest,
-                    args.apply_sample, args.perturb, log=lambda m: print(f"{args.impl}: {m}", flush=True))
+                    args.apply_sample, args.perturb_seed, log=lambda m: print(f"{args.impl}: {m}", flush=True))
     out = args.out or os.path.join(ROOT, "gpurun_out", f"digest_{args.impl}_c{args.cid}_{blob['method']}.npz")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     np.savez_compressed(out, **blob)

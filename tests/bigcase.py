@@ -17,7 +17,7 @@ from paper_1912_04385_b200 import gen
 X_STRIDE = 97
 APPLY_STRIDE = 997
 SCALARS = ("setup_s", "solve_s", "iterations", "total_iterations", "attempts", "converged", "breakdown",
-           "final_true_residual", "x_norm", "x_err_vs_xstar", "apply_norm", "perturb")
+           "final_true_residual", "x_norm", "x_err_vs_xstar", "apply_norm", "perturb_seed")
 
 
 def digest(a) -> str:
@@ -46,14 +46,15 @@ def setup_digests(s) -> dict:
     return out
 
 
-def run_case(api, cid, iters=500, method=None, setup_digest=True, apply_sample=False, perturb=0.0, log=print):
+def run_case(api, cid, iters=500, method=None, setup_digest=True, apply_sample=False, perturb_seed=None, log=print):
     import time
     method = method or gen.CONFIG_METHODS[cid][-1]
     a, b, xs = gen.generate(cid)
     blob = {"input": digest(a.values) + digest(b), "method": method}
-    if perturb:
-        b = b * (1.0 + perturb * np.random.default_rng(12345).standard_normal(b.size))
-        blob["perturb"] = perturb
+    if perturb_seed is not None:  # rounding-level perturbation of b (tests/ensemble.py)
+        from tests.ensemble import perturbed
+        b = perturbed(b, perturb_seed)
+        blob["perturb_seed"] = perturb_seed
     s = api.system(a)
     a.values = None  # the implementation holds its own copy (host RAM for the oracle at c5)
     t0 = time.time()

@@ -7,10 +7,11 @@ reference's own execution by tests/test_ref_pin.py.
 
     python tests/golden/make_big_golden.py [4] [5]
 
-Cost in this container (1 core): c4 ~4 min (three attempts of ~75
-iterations); c5 ~12 min (67 s setup, 40 iterations of ~15 s, ~45 GB RAM), plus
-the same c5 run with b perturbed by 1e-15 (N(0,1) relative): the history's own
-sensitivity to rounding-level changes.
+Each record also holds the same solve with b perturbed by 1e-15 (N(0,1)
+relative; tests/ensemble.py) -- 3 runs at c4, 1 at c5 --: the oracle's own
+sensitivity to rounding-level changes, the band the GPU is held to.
+Cost in this container (1 core): c4 ~16 min (4 x three attempts of ~75
+iterations); c5 ~25 min (2 x (67 s setup + 40 iterations of ~15 s), ~45 GB RAM).
 """
 import os
 import sys
@@ -25,17 +26,24 @@ import oracle  # noqa: E402
 from tests.bigcase import run_case  # noqa: E402
 
 C5_ITERS = 40
+C4_PERTURBED = 3
+C5_PERTURBED = 1
 
 
 def main(cids):
     o = oracle.api()
     for cid in cids:
-        if cid == 4:
-            blob = run_case(o, 4, 500, apply_sample=True)
-        else:
-            blob = run_case(o, 5, C5_ITERS, apply_sample=True)
-            pert = run_case(o, 5, C5_ITERS, setup_digest=False, perturb=1e-15)
-            blob["perturbed_history"] = pert["history"]
+        iters, npert = (500, C4_PERTURBED) if cid == 4 else (C5_ITERS, C5_PERTURBED)
+        blob = run_case(o, cid, iters, apply_sample=True)
+        # the oracle's own rounding band (tests/ensemble.py): the same solve with
+        # b perturbed by 1e-15
+        for s in range(npert):
+            pert = run_case(o, cid, iters, setup_digest=False, perturb_seed=s)
+            blob[f"pert{s}_history"] = pert["history"]
+            blob[f"pert{s}_attempt_iterations"] = pert["attempt_iterations"]
+            blob[f"pert{s}_final_true_residual"] = pert["final_true_residual"]
+            blob[f"pert{s}_attempt_true_residual"] = pert["attempt_true_residual"]
+            blob[f"pert{s}_x_sample"] = pert["x_sample"]
         np.savez_compressed(os.path.join(HERE, f"big_c{cid}.npz"), **blob)
         print(f"c{cid}: iterations {blob['iterations']} attempts {blob['attempts']}", flush=True)
 
