@@ -24,6 +24,7 @@ system, no collective on the data path; rank 0 prints the JSON line.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -287,6 +288,15 @@ def ours(args):
         api.call("kernel_stats", s.h, k, C.byref(t), C.byref(n), C.byref(by))
         stats[name] = {"ms": t.value, "launches": n.value, "bytes": by.value}
     api.call("profile", s.h, 0)
+    # the last timed solve's residual history: final scaled residual + digest, so
+    # the endpoint can be compared with the oracle's trajectory (tests/golden/big_c5.npz)
+    hl = C.c_int()
+    api.call("last_history", s.h, None, 0, C.byref(hl))
+    hist = np.zeros(max(hl.value, 1))
+    api.call("last_history", s.h, _ptr(hist), hist.size, C.byref(hl))
+    info["final_scaled_residual"] = float(hist[hl.value - 1]) if hl.value else None
+    info["history_sha256_16"] = hashlib.sha256(hist[:hl.value].tobytes()).hexdigest()[:16]
+    info["history_at"] = {str(k): float(hist[k]) for k in (1, 2, 12, 40, 100, 200, 300, 400, 500) if k < hl.value}
     from paper_1912_04385_b200 import replicas
     ms = replicas.reduce_max(ms, dev)
     value = replicas.reduce_sum(tot_it, dev) / (ms / 1e3)

@@ -189,6 +189,11 @@ int mprec_gpu_solve(mprec_gpu_system* h, double tol, int max_iter, double* x,
 int mprec_gpu_solve_dev(mprec_gpu_system* h, double tol, int max_iter, double* x_dev,
                         mprec_solve_result* out);
 
+/* Residual history (SolveResult::residual_history, gmres.hpp:31) of the last
+ * solve on the handle's last attempt: up to history_cap entries into history
+ * (may be NULL), the full length into *len. */
+int mprec_gpu_last_history(mprec_gpu_system* h, double* history, int history_cap, int* len);
+
 /* Whole solve_system (harness.cpp:190-219) from host buffers: create + setup
  * + solve + destroy. */
 int mprec_gpu_solve_system(const mprec_bsr* a, const double* b, int method, double tol,

@@ -289,6 +289,7 @@ class Api:
             "get_levelsets": (C.c_int, [vp, C.c_int, vp, ip]),
             "amg_get_levelsets": (C.c_int, [vp, C.c_int, C.c_int, vp, ip]),
             "solve_dev": (C.c_int, [vp, C.c_double, C.c_int, vp, vp]),
+            "last_history": (C.c_int, [vp, vp, C.c_int, vp]),
             "solve_system": (C.c_int, [vp, vp, C.c_int, C.c_double, C.c_int, vp, vp]),
             "device_info": (C.c_int, [ip, ip, ip, i64p]),
             "profile": (C.c_int, [vp, C.c_int]),

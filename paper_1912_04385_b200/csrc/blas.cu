@@ -48,8 +48,9 @@ cudaEvent_t Ctx::get_event() {
     return e;
 }
 
-Ctx::Scope::Scope(Ctx* c_, int kc_, double bytes_) : c(c_), kc(kc_), bytes(bytes_) {
+Ctx::Scope::Scope(Ctx* c_, int kc_, double bytes_, bool gated_) : c(c_), kc(kc_), bytes(bytes_), gated(gated_) {
     c->launches++;
+    if (gated) c->unresolved_gated++;
     if (c->profile) {
         a = c->get_event();
         cudaEventRecord(a, c->s);
@@ -60,12 +61,28 @@ Ctx::Scope::~Scope() {
     if (a) {
         cudaEvent_t b = c->get_event();
         cudaEventRecord(b, c->s);
-        c->pending.push_back({kc, bytes, a, b});
-        if (c->pending.size() > 4096) c->harvest();
+        c->pending.push_back({kc, bytes, a, b, gated});
+        if (c->pending.size() > 4096 && c->unresolved_gated == 0) c->harvest();
     } else {
         c->stat[kc].launches++;
-        c->stat[kc].bytes += bytes;
+        if (gated)
+            c->gated_bytes[kc] += bytes;
+        else
+            c->stat[kc].bytes += bytes;
     }
+}
+
+void Ctx::resolve_gate(bool fired) {
+    for (auto& p : pending)
+        if (p.gated) {
+            if (!fired) p.bytes = 0.0;
+            p.gated = false;
+        }
+    for (int k = 0; k < MPREC_K_COUNT; ++k) {
+        if (fired) stat[k].bytes += gated_bytes[k];
+        gated_bytes[k] = 0.0;
+    }
+    unresolved_gated = 0;
 }
 
 void Ctx::harvest() {

@@ -118,6 +118,16 @@ struct Krylov {
     DBuf<double> gt, pbuf, part;  // transposed Gram lower part, coefficients, pass-A partials
 };
 
+// MPREC_GRAM_FUSED=1: re-orthogonalisation pass A fused into pass B (opt-in:
+// measured slower at c5)
+static bool gram_fused() {
+    static const bool on = [] {
+        const char* e = getenv("MPREC_GRAM_FUSED");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // gmres.cpp:8-106 over device vectors.  b, x: device; n unknowns.
 GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M, const double* b, double tol,
                    int max_iter, double* x) {
@@ -166,17 +176,24 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
         double* hc = kr.hcol.p;
         // MGS (gmres.cpp:39-42) in Gram form (gram.cu): V^T w and the basis' new
         // Gram row in one pass, (I + L) h = V^T w, w -= V h in a second pass
-        gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, false, k > 0, sc + 1, sc + 2, kr.part.p, nullptr);
-        // one re-orthogonalisation pass when ||w|| < 0.7 pre_norm (gmres.cpp:44-50), gated on device
-        set_reorth_gate(c, sc + 2, sc + 1, gate);
-        gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, true, false, nullptr, sc + 3, kr.part.p, gate);
+        // one re-orthogonalisation pass when ||w|| < 0.7 pre_norm (gmres.cpp:44-50), gated on
+        // device; its pass A is fused into the first sweep's pass B (gram_orthogonalise)
+        if (gram_fused()) {
+            gram_orthogonalise(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, sc + 1, sc + 2, sc + 3, kr.part.p, gate);
+        } else {
+            gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, false, k > 0, sc + 1, sc + 2, kr.part.p, nullptr);
+            set_reorth_gate(c, sc + 2, sc + 1, gate);
+            gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, true, false, nullptr, sc + 3, kr.part.p, gate);
+        }
         // read back the Hessenberg column
         MG_CUDA(cudaMemcpyAsync(col.data(), hc, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c.s));
         double tail[3];
         int gh = 0;
         MG_CUDA(cudaMemcpyAsync(tail, sc + 1, sizeof(double) * 3, cudaMemcpyDeviceToHost, c.s));
         MG_CUDA(cudaMemcpyAsync(&gh, gate, sizeof(int), cudaMemcpyDeviceToHost, c.s));
-        c.sync();
+        MG_CUDA(cudaStreamSynchronize(c.s));
+        c.resolve_gate(gh != 0);  // charge the re-orthogonalisation's bytes only when it ran
+        if (!c.pending.empty() && c.pending.size() > 2048) c.harvest();
         for (int i = 0; i <= k; ++i) H(i, k) = col[i];
         H(k + 1, k) = gh ? tail[2] : tail[1];
         const double subdiag = H(k + 1, k);
@@ -472,8 +489,10 @@ struct mprec_gpu_system {
             opt_tol *= 0.5 * tol / res.final_true_residual;
         }
         if (res.converged && res.final_true_residual > tol) res.converged = false;
+        last_history = res.history;
         return res;
     }
+    std::vector<double> last_history;  // residual history of the last solve's last attempt
 };
 
 extern "C" {
@@ -814,6 +833,16 @@ int mprec_gpu_solve_dev(mprec_gpu_system* h, double tol, int max_iter, double* x
         h->ctx.sync();
         fill_result(out, g, attempts, h->setup_s, now_s() - t0, nullptr, 0, h->total_iterations);
         h->log_attempts(out);
+    });
+}
+
+int mprec_gpu_last_history(mprec_gpu_system* h, double* history, int history_cap, int* len) {
+    return guard([&] {
+        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
+        const int m = int(h->last_history.size());
+        if (len) *len = m;
+        if (history)
+            for (int i = 0; i < std::min(m, history_cap); ++i) history[i] = h->last_history[i];
     });
 }
 

@@ -139,6 +139,7 @@ struct Ctx {
         int kc;
         double bytes;
         cudaEvent_t a, b;
+        bool gated;  // launched under a device gate not yet resolved (resolve_gate)
     };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -155,14 +156,21 @@ struct Ctx {
 
     cudaEvent_t get_event();
     // Bracket a launch of kernel class kc with algorithmic byte count `bytes`.
+    // gated: the kernel exits at once unless a device flag is set; its bytes are
+    // held back until the host learns the flag (resolve_gate) and charged only
+    // when it fired.
     struct Scope {
         Ctx* c;
         int kc;
         double bytes;
+        bool gated;
         cudaEvent_t a = nullptr;
-        Scope(Ctx* c_, int kc_, double bytes_);
+        Scope(Ctx* c_, int kc_, double bytes_, bool gated_ = false);
         ~Scope();
     };
+    double gated_bytes[MPREC_K_COUNT] = {};  // non-profiling mode: held-back bytes
+    int unresolved_gated = 0;
+    void resolve_gate(bool fired);
     void harvest();  // fold completed event pairs into stat (synchronizes)
     void sync() {
         MG_CUDA(cudaStreamSynchronize(s));

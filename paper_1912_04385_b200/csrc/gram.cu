@@ -262,6 +262,121 @@ __global__ void __launch_bounds__(kGT) k_gram_b(const double* const* __restrict_
     *ctr = 0;
 }
 
+// Pass B of the first MGS sweep fused with pass A of the (gated) re-orthogonalisation
+// sweep: w' = w - V c, ||w'||, and the per-block partials of p' = V^T w', reading the
+// basis ONCE from HBM.  A block takes row sub-tiles of kBR rows; each of its four
+// quarters (two warps, one row per lane) owns every fourth storage chunk.  Phase 1
+// streams the sub-tile's rows of all k + 1 vectors from HBM and forms the quarter's
+// part of V c; the quarters combine it into w' in shared memory; phase 2 re-reads the
+// same rows -- in reverse chunk order, so the most recently streamed lines come first
+// -- from L2 (the grid is sized so that every block's sub-tile working set,
+// kBR (k + 1) 8 bytes, fits L2 together) and accumulates v_i . w' per warp.  The
+// speculative p' costs L2 reads only; the sweep that uses it runs only when the gate
+// fires (gmres.cpp:44-50).  Deterministic: per-warp accumulators, fixed orders.
+constexpr int kBR = 64;  // rows per sub-tile
+constexpr int kBQ = 4;   // chunk quarters
+
+__device__ __forceinline__ int butterfly8(double (&vv)[kGV], int lane) {
+    int idx = 0;
+#pragma unroll
+    for (int cnt = kGV, o = 16; cnt > 1; cnt /= 2, o /= 2) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i = 0; i < cnt / 2; ++i) {
+            const double send = up ? vv[i] : vv[i + cnt / 2];
+            const double keep = up ? vv[i + cnt / 2] : vv[i];
+            vv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        if (up) idx += cnt / 2;
+    }
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) vv[0] += __shfl_xor_sync(0xffffffffu, vv[0], o);
+    return idx;  // valid on lanes with (lane & 3) == 0
+}
+
+__global__ void __launch_bounds__(kGT) k_gram_ba(const double* const* __restrict__ ct, int k,
+                                                  const double* __restrict__ cvec, double* __restrict__ w, int64_t n,
+                                                  double* __restrict__ part, int stride, double* npart, unsigned* ctr,
+                                                  double* norm_out) {
+    extern __shared__ double sm[];
+    double* cs = sm;                        // k + 1 coefficients
+    double* acc = cs + (k + 1);             // [8 warps][k + 1] dot accumulators
+    double* xq = acc + 8 * (k + 1);         // [kBQ][kBR] phase-1 partials
+    double* red = xq + kBQ * kBR;           // [8]
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int q = wid >> 1, rr = (wid & 1) * 32 + lane;
+    for (int i = tid; i <= k; i += kGT) cs[i] = cvec[i];
+    for (int i = tid; i < 8 * (k + 1); i += kGT) acc[i] = 0.0;
+    __syncthreads();
+    double* myacc = acc + wid * (k + 1);
+    const int ck = k / kGV, jk = k % kGV;
+    const int64_t nsub = (n + kBR - 1) / kBR;
+    double ss = 0.0;
+    for (int64_t st = blockIdx.x; st < nsub; st += gridDim.x) {
+        const int64_t r = st * kBR + rr;
+        const bool in = r < n;
+        const int64_t tile = (st * kBR) / kT;
+        const int off = int((st * kBR) % kT) + rr;
+        // phase 1: this quarter's part of V c for row r (HBM stream)
+        double xa = 0.0;
+        for (int c = q; c <= ck; c += kBQ) {
+            const double* base = tile_base(ct, c, tile) + off;
+            const int nv = c < ck ? kGV : jk + 1;
+#pragma unroll
+            for (int j = 0; j < kGV; ++j)
+                if (j < nv && in) xa += cs[c * kGV + j] * __ldcg(base + j * kT);
+        }
+        xq[q * kBR + rr] = xa;
+        __syncthreads();
+        double x = 0.0;
+        if (in) {
+            x = w[r] - ((xq[rr] + xq[kBR + rr]) + (xq[2 * kBR + rr] + xq[3 * kBR + rr]));
+            if (q == 0) {
+                w[r] = x;
+                ss += x * x;
+            }
+        }
+        // phase 2: v_i . w' (L2), newest chunks first
+        const int clast = ck - ((ck - q) % kBQ + kBQ) % kBQ;  // largest c <= ck with c = q (mod kBQ)
+        for (int c = clast; c >= q; c -= kBQ) {
+            const double* base = tile_base(ct, c, tile) + off;
+            const int nv = c < ck ? kGV : jk + 1;
+            double vv[kGV];
+#pragma unroll
+            for (int j = 0; j < kGV; ++j) vv[j] = (j < nv && in) ? __ldcg(base + j * kT) * x : 0.0;
+            const int idx = butterfly8(vv, lane);
+            if ((lane & 3) == 0 && c * kGV + idx <= k) myacc[c * kGV + idx] += vv[0];
+        }
+        __syncthreads();  // xq reused by the next sub-tile
+    }
+    // per-block partials of p' (warps summed in a fixed order); entries k+1.. unused
+    for (int i = tid; i <= k; i += kGT) {
+        double s = 0.0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) s += acc[v * (k + 1) + i];
+        part[int64_t(blockIdx.x) * stride + i] = s;
+    }
+    // ||w'||: block partials, the last block sums them in block order
+    ss = warp_sum(ss);
+    if (lane == 0) red[wid] = ss;
+    __syncthreads();
+    __shared__ bool last;
+    if (tid == 0) {
+        double s = 0.0;
+        for (int v = 0; v < kGT / 32; ++v) s += red[v];
+        npart[blockIdx.x] = s;
+        __threadfence();
+        last = atomicInc(ctr, 0xFFFFFFFFu) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || tid != 0) return;
+    __threadfence();
+    double s = 0.0;
+    for (int b = 0; b < int(gridDim.x); ++b) s += reinterpret_cast<volatile double*>(npart)[b];
+    *norm_out = sqrt(s);
+    *ctr = 0;
+}
+
 __global__ void k_set_ptr(double** tab, int i, double* p) { tab[i] = p; }
 
 // vector j of a chunk <- x / a (put) or y <- vector j of a chunk (get)
@@ -308,7 +423,7 @@ void gram_sweep(Ctx& c, const double* const* ct, int k, double* w, int64_t n, do
     const int stride = 2 * (k + 1) + 1;
     const int grid_a = tile_grid(c, n, 4);
     {
-        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 2));
+        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 2), gate != nullptr);
         const size_t smem = sizeof(double) * (stride + (kGT / 32) * kGRed);
         static size_t attr = 0;
         if (smem > 48 * 1024 && smem > attr) {
@@ -323,18 +438,18 @@ void gram_sweep(Ctx& c, const double* const* ct, int k, double* w, int64_t n, do
         check_launch("gram pass A");
     }
     {
-        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * grid_a * stride);
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * grid_a * stride, gate != nullptr);
         k_gram_fin<<<(stride + 7) / 8, 256, 0, c.s>>>(part, grid_a, stride, k, pbuf, gt, ld, pre_norm,
                                                       want_q ? 1 : 0, gate);
         check_launch("gram fin");
     }
     {
-        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * (k + 1) * (k + 1) / 2);
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * (k + 1) * (k + 1) / 2, gate != nullptr);
         k_gram_tri<<<1, 512, sizeof(double) * (k + 1), c.s>>>(gt, ld, k, pbuf, h, accumulate ? 1 : 0, gate);
         check_launch("gram tri");
     }
     {
-        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 3));
+        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 3), gate != nullptr);
         const size_t smem = sizeof(double) * (k + 1 + kGT / 32);
         static size_t attr = 0;
         if (smem > 48 * 1024 && smem > attr) {
@@ -344,6 +459,85 @@ void gram_sweep(Ctx& c, const double* const* ct, int k, double* w, int64_t n, do
         const int grid_b = std::min(tile_grid(c, n, 8), kRedBlocks);
         k_gram_b<<<grid_b, kGT, smem, c.s>>>(ct, k, pbuf, w, n, c.red.p, c.red_ctr.p + 8, post_norm, 0, gate);
         check_launch("gram pass B");
+    }
+}
+
+// One Arnoldi orthogonalisation (gmres.cpp:37-51) with the re-orthogonalisation's
+// pass A fused into the first sweep's pass B (k_gram_ba): pass A, (I+L) h = p,
+// [w -= V h, ||w||, p' = V^T w], gate, then -- gated -- (I+L) c = p', h += c,
+// w -= V c, ||w||.  Three reads of the basis from HBM when the gate fires (four with
+// gram_sweep twice), two when it does not.
+void gram_orthogonalise(Ctx& c, const double* const* ct, int k, double* w, int64_t n, double* gt, int ld,
+                        double* pbuf, double* h, double* pre_norm, double* post_norm, double* reorth_norm,
+                        double* part, int* gate) {
+    const int stride = 2 * (k + 1) + 1;
+    const int grid_a = tile_grid(c, n, 4);
+    {
+        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 2));
+        const size_t smem = sizeof(double) * (stride + (kGT / 32) * kGRed);
+        static size_t attr = 0;
+        if (smem > 48 * 1024 && smem > attr) {
+            MG_CUDA(cudaFuncSetAttribute(k_gram_a<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            MG_CUDA(cudaFuncSetAttribute(k_gram_a<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr = smem;
+        }
+        if (k > 0)
+            k_gram_a<true><<<grid_a, kGT, smem, c.s>>>(ct, k, w, n, part, stride, 1, nullptr);
+        else
+            k_gram_a<false><<<grid_a, kGT, smem, c.s>>>(ct, k, w, n, part, stride, 0, nullptr);
+        check_launch("gram pass A");
+    }
+    {
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * grid_a * stride);
+        k_gram_fin<<<(stride + 7) / 8, 256, 0, c.s>>>(part, grid_a, stride, k, pbuf, gt, ld, pre_norm, k > 0 ? 1 : 0,
+                                                      nullptr);
+        check_launch("gram fin");
+    }
+    {
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * (k + 1) * (k + 1) / 2);
+        k_gram_tri<<<1, 512, sizeof(double) * (k + 1), c.s>>>(gt, ld, k, pbuf, h, 0, nullptr);
+        check_launch("gram tri");
+    }
+    // fused pass B + speculative pass A': blocks whose sub-tile working sets fit L2
+    const int64_t nsub = (n + kBR - 1) / kBR;
+    const double ws = double(kBR) * (k + 1) * 8.0;
+    const int grid_ba = int(std::max<int64_t>(1, std::min<int64_t>({nsub, int64_t(2) * c.sm_count,
+                                                                     std::max<int64_t>(c.sm_count, int64_t(64e6 / ws)),
+                                                                     kRedBlocks})));
+    {
+        // algorithmic: basis once + w read and written; the L2 re-read is not charged
+        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 3));
+        const size_t smem = sizeof(double) * (9 * (k + 1) + kBQ * kBR + 8);
+        static size_t attr = 0;
+        if (smem > 48 * 1024 && smem > attr) {
+            MG_CUDA(cudaFuncSetAttribute(k_gram_ba, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr = smem;
+        }
+        k_gram_ba<<<grid_ba, kGT, smem, c.s>>>(ct, k, pbuf, w, n, part, stride, c.red.p, c.red_ctr.p + 8, post_norm);
+        check_launch("gram pass BA");
+    }
+    set_reorth_gate(c, post_norm, pre_norm, gate);
+    {
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * grid_ba * (k + 1), true);
+        k_gram_fin<<<(stride + 7) / 8, 256, 0, c.s>>>(part, grid_ba, stride, k, pbuf, gt, ld, nullptr, 0, gate);
+        check_launch("gram fin (reorth)");
+    }
+    {
+        Ctx::Scope sc(&c, MPREC_K_BLAS1, 8.0 * (k + 1) * (k + 1) / 2, true);
+        k_gram_tri<<<1, 512, sizeof(double) * (k + 1), c.s>>>(gt, ld, k, pbuf, h, 1, gate);
+        check_launch("gram tri (reorth)");
+    }
+    {
+        Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 3), true);
+        const size_t smem = sizeof(double) * (k + 1 + kGT / 32);
+        static size_t attr = 0;
+        if (smem > 48 * 1024 && smem > attr) {
+            MG_CUDA(cudaFuncSetAttribute(k_gram_b, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            attr = smem;
+        }
+        const int grid_b = std::min(tile_grid(c, n, 8), kRedBlocks);
+        k_gram_b<<<grid_b, kGT, smem, c.s>>>(ct, k, pbuf, w, n, c.red.p, c.red_ctr.p + 8, reorth_norm, 0, gate);
+        check_launch("gram pass B (reorth)");
     }
 }
 

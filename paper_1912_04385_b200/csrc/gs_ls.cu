@@ -951,7 +951,8 @@ void gs_ls_experiment(Ctx& c, Amg& amg, int l, int K, int reps, double* out) {
         long long t0 = h[0];
         for (int g = 0; g < sf.K; ++g) t0 = std::min(t0, h[4 * g]);
         fprintf(stderr, "[ls stats] level n=%d K=%d (group: start end wait_us waits chunks)\n", n, sf.K);
-        for (int g = 0; g < sf.K; g += std::max(1, sf.K / 12))
+        const int every = atoi(getenv("MPREC_LS_STATS")) >= 2 ? 1 : std::max(1, sf.K / 12);
+        for (int g = 0; g < sf.K; g += every)
             fprintf(stderr, "  g%3d: %8.1f %8.1f %8.1f %6lld %5d\n", g, (h[4 * g] - t0) * 1e-3, (h[4 * g + 1] - t0) * 1e-3,
                     h[4 * g + 2] * 1e-3, h[4 * g + 3], gch[g].y);
     }

@@ -96,6 +96,9 @@ void basis_put(Ctx& c, double* chunk, int j, const double* x, double a, int64_t 
 void basis_get(Ctx& c, double* y, const double* chunk, int j, int64_t n);
 void basis_combine(Ctx& c, const double* const* ct, int k, const double* y, double* z, int64_t n);  // z = V_k y
 int gram_part_size(Ctx& c, int kmax);
+void gram_orthogonalise(Ctx& c, const double* const* ct, int k, double* w, int64_t n, double* gt, int ld,
+                        double* pbuf, double* h, double* pre_norm, double* post_norm, double* reorth_norm,
+                        double* part, int* gate);
 void gram_sweep(Ctx& c, const double* const* vt, int k, double* w, int64_t n, double* gt, int ld, double* pbuf,
                 double* h, bool accumulate, bool want_q, double* pre_norm, double* post_norm, double* part,
                 const int* gate);

@@ -44,6 +44,10 @@ def main(cids):
             blob[f"pert{s}_final_true_residual"] = pert["final_true_residual"]
             blob[f"pert{s}_attempt_true_residual"] = pert["attempt_true_residual"]
             blob[f"pert{s}_x_sample"] = pert["x_sample"]
+        if cid == 5:  # keep the committed record small: every 970th entry of x
+            for key in [k for k in blob if k.endswith("x_sample")]:
+                blob[key] = blob[key][::10]
+            blob["x_sample_stride"] = np.int64(970)
         np.savez_compressed(os.path.join(HERE, f"big_c{cid}.npz"), **blob)
         print(f"c{cid}: iterations {blob['iterations']} attempts {blob['attempts']}", flush=True)
 
