@@ -118,12 +118,11 @@ struct Krylov {
     DBuf<double> gt, pbuf, part;  // transposed Gram lower part, coefficients, pass-A partials
 };
 
-// MPREC_GRAM_FUSED=1: re-orthogonalisation pass A fused into pass B (opt-in:
-// measured slower at c5)
+// MPREC_GRAM_FUSED=0: the unfused two-sweep orthogonalisation (A/B experiments)
 static bool gram_fused() {
     static const bool on = [] {
         const char* e = getenv("MPREC_GRAM_FUSED");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }();
     return on;
 }
@@ -178,7 +177,7 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
         // Gram row in one pass, (I + L) h = V^T w, w -= V h in a second pass
         // one re-orthogonalisation pass when ||w|| < 0.7 pre_norm (gmres.cpp:44-50), gated on
         // device; its pass A is fused into the first sweep's pass B (gram_orthogonalise)
-        if (gram_fused()) {
+        if (gram_fused() && k + 1 <= 512) {  // the fused pass holds <= 512 basis vectors per row in registers
             gram_orthogonalise(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, sc + 1, sc + 2, sc + 3, kr.part.p, gate);
         } else {
             gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, false, k > 0, sc + 1, sc + 2, kr.part.p, nullptr);

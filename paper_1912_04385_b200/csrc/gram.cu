@@ -264,97 +264,96 @@ __global__ void __launch_bounds__(kGT) k_gram_b(const double* const* __restrict_
 
 // Pass B of the first MGS sweep fused with pass A of the (gated) re-orthogonalisation
 // sweep: w' = w - V c, ||w'||, and the per-block partials of p' = V^T w', reading the
-// basis ONCE from HBM.  A block takes row sub-tiles of kBR rows; each of its four
-// quarters (two warps, one row per lane) owns every fourth storage chunk.  Phase 1
-// streams the sub-tile's rows of all k + 1 vectors from HBM and forms the quarter's
-// part of V c; the quarters combine it into w' in shared memory; phase 2 re-reads the
-// same rows -- in reverse chunk order, so the most recently streamed lines come first
-// -- from L2 (the grid is sized so that every block's sub-tile working set,
-// kBR (k + 1) 8 bytes, fits L2 together) and accumulates v_i . w' per warp.  The
-// speculative p' costs L2 reads only; the sweep that uses it runs only when the gate
-// fires (gmres.cpp:44-50).  Deterministic: per-warp accumulators, fixed orders.
-constexpr int kBR = 64;  // rows per sub-tile
-constexpr int kBQ = 4;   // chunk quarters
+// basis ONCE.  The basis values a thread needs twice stay in its REGISTERS: a block
+// of 16 warps takes a row sub-tile; warp (vector group vg, row set rs) holds, lane =
+// row, the values of <= 32 consecutive basis vectors (vg*32 ..) for its 32 rows.
+//   phase 1: per-warp partial of (V c)[row] over its 32 vectors; the NG partials of
+//            a row are combined in shared memory in group order: x = w - V c;
+//   phase 2: v_j[row] * x[row] for the same 32 register values, reduced over the
+//            32 rows of the warp by one butterfly (31 shuffles for 32 sums).
+// 32 independent 8-byte loads per thread, 128 KB in flight per SM (one block per
+// SM, persistent).  The speculative p' costs no extra memory traffic; the sweep that
+// uses it runs only when the gate fires (gmres.cpp:44-50).  Deterministic: per-warp
+// accumulators, fixed orders.
+constexpr int kBW = 16;  // warps per block
 
-__device__ __forceinline__ int butterfly8(double (&vv)[kGV], int lane) {
-    int idx = 0;
-#pragma unroll
-    for (int cnt = kGV, o = 16; cnt > 1; cnt /= 2, o /= 2) {
-        const bool up = lane & o;
-#pragma unroll
-        for (int i = 0; i < cnt / 2; ++i) {
-            const double send = up ? vv[i] : vv[i + cnt / 2];
-            const double keep = up ? vv[i + cnt / 2] : vv[i];
-            vv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-        if (up) idx += cnt / 2;
-    }
-#pragma unroll
-    for (int o = 2; o > 0; o >>= 1) vv[0] += __shfl_xor_sync(0xffffffffu, vv[0], o);
-    return idx;  // valid on lanes with (lane & 3) == 0
-}
-
-__global__ void __launch_bounds__(kGT) k_gram_ba(const double* const* __restrict__ ct, int k,
-                                                  const double* __restrict__ cvec, double* __restrict__ w, int64_t n,
-                                                  double* __restrict__ part, int stride, double* npart, unsigned* ctr,
-                                                  double* norm_out) {
-    extern __shared__ double sm[];
-    double* cs = sm;                        // k + 1 coefficients
-    double* acc = cs + (k + 1);             // [8 warps][k + 1] dot accumulators
-    double* xq = acc + 8 * (k + 1);         // [kBQ][kBR] phase-1 partials
-    double* red = xq + kBQ * kBR;           // [8]
+template <int NG>  // vector groups of 32: NG = next power of two >= (k + 1) / 32
+__global__ void __launch_bounds__(kBW * 32, 1) k_gram_ba(const double* const* __restrict__ ct, int k,
+                                                          const double* __restrict__ cvec, double* __restrict__ w,
+                                                          int64_t n, double* __restrict__ part, int stride,
+                                                          double* npart, unsigned* ctr, double* norm_out) {
+    constexpr int NRS = kBW / NG;  // row sets of 32 rows per sub-tile
+    constexpr int R = 32 * NRS;    // rows per sub-tile (divides kT)
+    __shared__ double cs[32 * NG];
+    __shared__ double xp[NG][R];
+    __shared__ double xs[R];
+    __shared__ double acc[kBW][32];
+    __shared__ double red[kBW];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int q = wid >> 1, rr = (wid & 1) * 32 + lane;
-    for (int i = tid; i <= k; i += kGT) cs[i] = cvec[i];
-    for (int i = tid; i < 8 * (k + 1); i += kGT) acc[i] = 0.0;
+    const int vg = wid % NG, rs = wid / NG;
+    for (int i = tid; i < 32 * NG; i += blockDim.x) cs[i] = i <= k ? cvec[i] : 0.0;
+    acc[wid][lane] = 0.0;
     __syncthreads();
-    double* myacc = acc + wid * (k + 1);
-    const int ck = k / kGV, jk = k % kGV;
-    const int64_t nsub = (n + kBR - 1) / kBR;
+    const int j0 = vg * 32;
+    const int nv = max(0, min(32, k + 1 - j0));
+    const double* cbase[4];  // the group's 4 storage chunks
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cbase[q] = (j0 / kGV + q) * kGV <= k ? ct[j0 / kGV + q] : nullptr;
+    const int64_t nsub = (n + R - 1) / R;
     double ss = 0.0;
     for (int64_t st = blockIdx.x; st < nsub; st += gridDim.x) {
-        const int64_t r = st * kBR + rr;
-        const bool in = r < n;
-        const int64_t tile = (st * kBR) / kT;
-        const int off = int((st * kBR) % kT) + rr;
-        // phase 1: this quarter's part of V c for row r (HBM stream)
-        double xa = 0.0;
-        for (int c = q; c <= ck; c += kBQ) {
-            const double* base = tile_base(ct, c, tile) + off;
-            const int nv = c < ck ? kGV : jk + 1;
+        const int64_t row = st * R + rs * 32 + lane;
+        const bool in = row < n;
+        const int64_t tile = (st * R) / kT;
+        const int off = int((st * R) % kT) + rs * 32 + lane;
+        double v[32];
 #pragma unroll
-            for (int j = 0; j < kGV; ++j)
-                if (j < nv && in) xa += cs[c * kGV + j] * __ldcg(base + j * kT);
+        for (int t = 0; t < 32; ++t)
+            v[t] = (t < nv && in) ? __ldcs(cbase[t / kGV] + tile * (int64_t(kGV) * kT) + (t % kGV) * kT + off) : 0.0;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+            a0 = fma(cs[j0 + t], v[t], a0);
+            a1 = fma(cs[j0 + t + 1], v[t + 1], a1);
         }
-        xq[q * kBR + rr] = xa;
+        xp[vg][rs * 32 + lane] = a0 + a1;
         __syncthreads();
-        double x = 0.0;
-        if (in) {
-            x = w[r] - ((xq[rr] + xq[kBR + rr]) + (xq[2 * kBR + rr] + xq[3 * kBR + rr]));
-            if (q == 0) {
-                w[r] = x;
+        if (vg == 0) {
+            double vc = 0.0;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) vc += xp[g][rs * 32 + lane];
+            const double x = in ? w[row] - vc : 0.0;
+            xs[rs * 32 + lane] = x;
+            if (in) {
+                w[row] = x;
                 ss += x * x;
             }
         }
-        // phase 2: v_i . w' (L2), newest chunks first
-        const int clast = ck - ((ck - q) % kBQ + kBQ) % kBQ;  // largest c <= ck with c = q (mod kBQ)
-        for (int c = clast; c >= q; c -= kBQ) {
-            const double* base = tile_base(ct, c, tile) + off;
-            const int nv = c < ck ? kGV : jk + 1;
-            double vv[kGV];
+        __syncthreads();
+        const double x = xs[rs * 32 + lane];
 #pragma unroll
-            for (int j = 0; j < kGV; ++j) vv[j] = (j < nv && in) ? __ldcg(base + j * kT) * x : 0.0;
-            const int idx = butterfly8(vv, lane);
-            if ((lane & 3) == 0 && c * kGV + idx <= k) myacc[c * kGV + idx] += vv[0];
+        for (int t = 0; t < 32; ++t) v[t] *= x;
+        int idx = 0;
+#pragma unroll
+        for (int cnt = 32, o = 16; cnt > 1; cnt /= 2, o /= 2) {
+            const bool up = lane & o;
+#pragma unroll
+            for (int i = 0; i < cnt / 2; ++i) {
+                const double send = up ? v[i] : v[i + cnt / 2];
+                const double keep = up ? v[i + cnt / 2] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+            if (up) idx += cnt / 2;
         }
-        __syncthreads();  // xq reused by the next sub-tile
+        acc[wid][idx] += v[0];
     }
-    // per-block partials of p' (warps summed in a fixed order); entries k+1.. unused
-    for (int i = tid; i <= k; i += kGT) {
-        double s = 0.0;
+    __syncthreads();
+    // per-block partials of p' (row sets summed in order); entries k+1.. unused
+    for (int j = tid; j <= k; j += blockDim.x) {
+        double sacc = 0.0;
 #pragma unroll
-        for (int v = 0; v < 8; ++v) s += acc[v * (k + 1) + i];
-        part[int64_t(blockIdx.x) * stride + i] = s;
+        for (int r2 = 0; r2 < NRS; ++r2) sacc += acc[r2 * NG + j / 32][j % 32];
+        part[int64_t(blockIdx.x) * stride + j] = sacc;
     }
     // ||w'||: block partials, the last block sums them in block order
     ss = warp_sum(ss);
@@ -362,18 +361,18 @@ __global__ void __launch_bounds__(kGT) k_gram_ba(const double* const* __restrict
     __syncthreads();
     __shared__ bool last;
     if (tid == 0) {
-        double s = 0.0;
-        for (int v = 0; v < kGT / 32; ++v) s += red[v];
-        npart[blockIdx.x] = s;
+        double sm2 = 0.0;
+        for (int v2 = 0; v2 < kBW; ++v2) sm2 += red[v2];
+        npart[blockIdx.x] = sm2;
         __threadfence();
         last = atomicInc(ctr, 0xFFFFFFFFu) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last || tid != 0) return;
     __threadfence();
-    double s = 0.0;
-    for (int b = 0; b < int(gridDim.x); ++b) s += reinterpret_cast<volatile double*>(npart)[b];
-    *norm_out = sqrt(s);
+    double tot = 0.0;
+    for (int b2 = 0; b2 < int(gridDim.x); ++b2) tot += reinterpret_cast<volatile double*>(npart)[b2];
+    *norm_out = sqrt(tot);
     *ctr = 0;
 }
 
@@ -498,22 +497,24 @@ void gram_orthogonalise(Ctx& c, const double* const* ct, int k, double* w, int64
         k_gram_tri<<<1, 512, sizeof(double) * (k + 1), c.s>>>(gt, ld, k, pbuf, h, 0, nullptr);
         check_launch("gram tri");
     }
-    // fused pass B + speculative pass A': blocks whose sub-tile working sets fit L2
-    const int64_t nsub = (n + kBR - 1) / kBR;
-    const double ws = double(kBR) * (k + 1) * 8.0;
-    const int grid_ba = int(std::max<int64_t>(1, std::min<int64_t>({nsub, int64_t(2) * c.sm_count,
-                                                                     std::max<int64_t>(c.sm_count, int64_t(64e6 / ws)),
-                                                                     kRedBlocks})));
+    // fused pass B + speculative pass A' (registers): one persistent block per SM
+    int grid_ba = 0;
     {
-        // algorithmic: basis once + w read and written; the L2 re-read is not charged
+        // algorithmic: basis once + w read and written
         Ctx::Scope sc(&c, MPREC_K_MGS, 8.0 * n * (k + 3));
-        const size_t smem = sizeof(double) * (9 * (k + 1) + kBQ * kBR + 8);
-        static size_t attr = 0;
-        if (smem > 48 * 1024 && smem > attr) {
-            MG_CUDA(cudaFuncSetAttribute(k_gram_ba, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-            attr = smem;
+        const int ng = k + 1 <= 32 ? 1 : k + 1 <= 64 ? 2 : k + 1 <= 128 ? 4 : k + 1 <= 256 ? 8 : 16;
+        if (k + 1 > 512) throw Error(MPREC_DIMENSION, "gram: fused pass supports k < 512");
+        const int R = 32 * (kBW / ng);
+        grid_ba = int(std::max<int64_t>(1, std::min<int64_t>((n + R - 1) / R, c.sm_count)));
+        auto* red = c.red.p;
+        auto* ctr = c.red_ctr.p + 8;
+        switch (ng) {
+            case 1: k_gram_ba<1><<<grid_ba, kBW * 32, 0, c.s>>>(ct, k, pbuf, w, n, part, stride, red, ctr, post_norm); break;
+            case 2: k_gram_ba<2><<<grid_ba, kBW * 32, 0, c.s>>>(ct, k, pbuf, w, n, part, stride, red, ctr, post_norm); break;
+            case 4: k_gram_ba<4><<<grid_ba, kBW * 32, 0, c.s>>>(ct, k, pbuf, w, n, part, stride, red, ctr, post_norm); break;
+            case 8: k_gram_ba<8><<<grid_ba, kBW * 32, 0, c.s>>>(ct, k, pbuf, w, n, part, stride, red, ctr, post_norm); break;
+            default: k_gram_ba<16><<<grid_ba, kBW * 32, 0, c.s>>>(ct, k, pbuf, w, n, part, stride, red, ctr, post_norm); break;
         }
-        k_gram_ba<<<grid_ba, kGT, smem, c.s>>>(ct, k, pbuf, w, n, part, stride, c.red.p, c.red_ctr.p + 8, post_norm);
         check_launch("gram pass BA");
     }
     set_reorth_gate(c, post_norm, pre_norm, gate);
