@@ -27,6 +27,11 @@
 #include <cub/cub.cuh>
 #include <cstdlib>
 
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include "mprec.cuh"
 
 namespace mg {
@@ -957,6 +962,30 @@ static void coarse_factor(Ctx& c, const CsrView& a, DBuf<double>& lu, DBuf<doubl
     c.sync();
 }
 
+// Sweep schedules of one smoothed level (run on the setup's helper thread).
+static void build_level_schedules(Ctx& c, AmgLevel& l, Pattern* pat) {
+    if (pat) {
+        pat->ensure_sched(c);  // (built before the hierarchies when two share it)
+        l.ofwd = pat->fwd.order.p;
+        l.obwd = pat->bwd.order.p;
+        l.glev_f = pat->fwd.level.p;
+        l.glev_b = pat->bwd.level.p;
+    } else {
+        build_sched(c, l.n, l.a.rp, l.a.ci, +1, l.own_fwd);
+        build_sched(c, l.n, l.a.rp, l.a.ci, -1, l.own_bwd);
+        l.ofwd = l.own_fwd.order.p;
+        l.obwd = l.own_bwd.order.p;
+        l.glev_f = l.own_fwd.level.p;
+        l.glev_b = l.own_bwd.level.p;
+    }
+    l.invd.alloc(std::max(l.n, 1));
+    compute_invd(c, l.a, l.invd.p);
+    l.b.ensure(std::max(l.n, 1));
+    l.xf.ensure(std::max(l.n, 1));
+    tune_level_sweep(c, l, pat ? pat->fwd : l.own_fwd, pat ? pat->bwd : l.own_bwd);
+    c.sync();
+}
+
 // AMGHierarchy::setup (amg.cpp:188-214)
 void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
     prm = p;
@@ -970,6 +999,47 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
         L0->a.diag = L0->a_own.diag.p;
     }
     lv.push_back(std::move(L0));
+    // Sweep schedules (Kahn levels, 1/a_ii, the level-synchronous programs) of a
+    // level are built on a helper thread with its own stream as soon as the level
+    // is known not to be the coarsest, i.e. while the single-warp RS first pass of
+    // the next level runs on this thread's stream (they only read the level).
+    Ctx cs;
+    std::mutex qm;
+    std::condition_variable qcv;
+    std::deque<std::pair<AmgLevel*, bool>> queue;  // (level, is level 0)
+    bool qdone = false;
+    std::exception_ptr qerr;
+    std::thread helper([&] {
+        StreamAllocScope alloc_on(cs.s);
+        try {
+            for (;;) {
+                std::pair<AmgLevel*, bool> job;
+                {
+                    std::unique_lock<std::mutex> lk(qm);
+                    qcv.wait(lk, [&] { return qdone || !queue.empty(); });
+                    if (queue.empty()) break;
+                    job = queue.front();
+                    queue.pop_front();
+                }
+                build_level_schedules(cs, *job.first, job.second ? pat : nullptr);
+            }
+            cs.sync();
+        } catch (...) {
+            qerr = std::current_exception();
+        }
+    });
+    auto finish_helper = [&] {
+        {
+            std::lock_guard<std::mutex> lk(qm);
+            qdone = true;
+        }
+        qcv.notify_one();
+        if (helper.joinable()) helper.join();
+    };
+    struct Joiner {  // the helper must not outlive this frame on an exception
+        std::function<void()> f;
+        ~Joiner() { f(); }
+    } joiner{finish_helper};
     while (lv.back()->n > prm.max_coarse && int(lv.size()) < prm.max_levels) {
         AmgLevel& f = *lv.back();
         auto nl = std::make_unique<AmgLevel>();
@@ -990,35 +1060,19 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
         diag_positions(c, nl->a, nl->a_own.diag);
         nl->a.diag = nl->a_own.diag.p;
         lv.push_back(std::move(nl));
+        {
+            std::lock_guard<std::mutex> lk(qm);
+            queue.emplace_back(lv[lv.size() - 2].get(), lv.size() == 2);
+        }
+        qcv.notify_one();
     }
     nco = lv.back()->n;
     Trace trc(&c, "amg coarse dense LU+inv");
     coarse_factor(c, lv.back()->a, coarse_lu, coarse_inv);
     {
-        Trace tr(&c, "amg sweep schedules");
-        for (size_t li = 0; li < lv.size(); ++li) {
-            AmgLevel& l = *lv[li];
-            if (li + 1 == lv.size()) break;  // the coarsest level is solved densely
-            if (li == 0 && pat) {
-                pat->ensure_sched(c);
-                l.ofwd = pat->fwd.order.p;
-                l.obwd = pat->bwd.order.p;
-                l.glev_f = pat->fwd.level.p;
-                l.glev_b = pat->bwd.level.p;
-            } else {
-                build_sched(c, l.n, l.a.rp, l.a.ci, +1, l.own_fwd);
-                build_sched(c, l.n, l.a.rp, l.a.ci, -1, l.own_bwd);
-                l.ofwd = l.own_fwd.order.p;
-                l.obwd = l.own_bwd.order.p;
-                l.glev_f = l.own_fwd.level.p;
-                l.glev_b = l.own_bwd.level.p;
-            }
-            l.invd.alloc(std::max(l.n, 1));
-            compute_invd(c, l.a, l.invd.p);
-            l.b.ensure(std::max(l.n, 1));
-            l.xf.ensure(std::max(l.n, 1));
-            tune_level_sweep(c, l, (li == 0 && pat) ? pat->fwd : l.own_fwd, (li == 0 && pat) ? pat->bwd : l.own_bwd);
-        }
+        Trace tr(&c, "amg sweep schedules (wait)");
+        finish_helper();
+        if (qerr) std::rethrow_exception(qerr);
     }
     {
         static const bool band_on = [] {
