@@ -1,21 +1,25 @@
-// ilu_ls.cu -- K6 v2: block ILU(0) triangular solves (ILU0Factor::apply,
-// ilu0.cpp:41-59) as a level-synchronous pipeline, nb = 8.
+// ilu_ls.cu -- K6 v3: block ILU(0) triangular solves (ILU0Factor::apply,
+// ilu0.cpp:41-59) as a level-synchronous pipeline over a SOLVE STREAM, nb = 8.
 //
-// The same mapping as the Gauss-Seidel programs (gs_ls.cu), on block rows: K
-// contiguous groups of block rows in sweep order, one thread block each; one
-// compute warp processes the group's block rows in block-DAG-level order, four
-// per step (lane = (block row b, scalar row r)), with only __syncwarp between
-// steps; the previous group's values arrive through an importer warp and a
-// shared-memory halo.  Per block row
-//     v   = rhs_I - sum_{dependency blocks K} B_IK y_K        (B = L or U block)
+// Mapping (as the Gauss-Seidel programs, gs_ls.cu): K contiguous groups of block
+// rows in sweep order, one thread block each.  Four compute warps process the
+// group's block rows in block-DAG-level order, up to 16 per step (lane = (block
+// row b, scalar row r)), a named barrier between steps; values of the group live
+// in a shared-memory ring, the previous group's values arrive through an
+// importer warp and a shared-memory halo ring.  Per block row
+//     v   = rhs_I - B0 y_K0 - B1 y_K1           (B = the L or U blocks of row I)
 //     y_I = inv(L_II) v (forward, unit lower)  /  inv(U_II) v (backward)
-// with the packed inverses of the diagonal blocks (k_ilu_dinv8).  The block
-// values are NOT copied into the program (they are the 10 GB factor): the
-// compute warp prefetches the blocks of the step P = 20 steps ahead straight
-// from the factor with 1-D TMA bulk copies (one per 512-byte block, completion
-// counted on one mbarrier per ring slot) into a shared-memory ring, so HBM
-// latency leaves the dependency chain.  The import halo is a ring
-// of 256 block rows; the importer is held back by the consumer's progress.
+// with the packed inverse of the diagonal block (k_ilu_dinv8).
+//
+// What makes it bandwidth-shaped: at factorisation the row's dependency blocks,
+// the packed inverse and a right-hand-side slot are copied into a per-direction
+// STREAM in processing order -- one step's data is one contiguous range -- so the
+// loader warp moves a whole step with ONE bulk copy (plus one for the step's
+// 272-byte metadata).  (The previous version gathered 16 separate 512-byte
+// blocks per step straight from the BSR factor: issue-bound, 28 ms per sweep at
+// c5.)  The right-hand side is scattered into the stream by a parallel pre-pass
+// per apply.  Results differ from the warp-per-block-row kernel (ilu_solve.cu)
+// only by association.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -28,15 +32,14 @@
 namespace mg {
 namespace {
 
-constexpr int kIB = 4;                   // block rows per step
-constexpr int kIStep = 16 + kIB * 24;    // program bytes per step
-constexpr int kISPC = kLsCH / kIStep;    // steps per program chunk
-constexpr int kIChunk = kISPC * kIStep;  // program chunk bytes
-constexpr int kIP = 20;                  // prefetch distance (steps)
+constexpr int kIB = 16;                  // block rows per step
+constexpr int kIRec = 200;               // doubles per row record: B0, B1, D, rhs
+constexpr int kIMeta = 16 + 16 * kIB;    // metadata bytes per step
+constexpr int kISlot = ((kIMeta + kIB * kIRec * 8) + 127) & ~127;  // ring slot bytes
+constexpr int kINS = 4;                  // ring slots
 constexpr int kIH = 256;                 // halo ring entries (block rows)
-constexpr int kIBlk = kIB * 200;         // doubles per prefetched step: 4 x (3 blocks + rhs)
-constexpr int kINS = 2;                  // program chunks in the ring
-constexpr int kIThreads = 96;
+constexpr int kICW = 4;                  // compute warps
+constexpr int kIThreads = 32 * (kICW + 2);
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
@@ -69,81 +72,51 @@ __device__ __forceinline__ unsigned long long ld_relaxed_il(const double* p) {
     return v;
 }
 
-// prefetch the blocks of one step into a ring slot with 1-D TMA bulk copies
-// (16 per step, lanes 0..15, completion counted on the slot's mbarrier): per
-// block row b, [0, 64) first dependency block, [64, 128) second, [128, 192) packed
-// inverse of the diagonal block, [192, 200) right-hand side.  Missing
-// dependencies read the zero block; padding block rows read the step's first
-// block row.  (16-byte cp.async per lane stalled at issue: 1.5 us per step.)
-__device__ __forceinline__ void il_prefetch(const int* rec, int lane, const double* __restrict__ val,
-                                            const double* __restrict__ dinv, const double* __restrict__ rhs,
-                                            const double* __restrict__ zero, double* slot, uint64_t* bar) {
-    if (lane == 0) mbar_expect_tx(bar, kIB * (3 * 512 + 64));
-    __syncwarp();
-    if (lane < 16) {
-        const int cnt = rec[0];
-        const int b = lane >> 2, w = lane & 3;
-        const int* br = rec + 4 + 6 * min(b, cnt - 1);
-        const int I = br[0];
-        const double* src;
-        unsigned bytes = 512;
-        if (w < 2) {
-            const int k = br[2 + w];
-            src = k >= 0 ? val + int64_t(k) * 64 : zero;
-        } else if (w == 2) {
-            src = dinv + int64_t(I) * 64;
-        } else {
-            src = rhs + int64_t(I) * 8;
-            bytes = 64;
-        }
-        bulk_g2s(slot + b * 200 + 64 * w, src, bytes, bar);
-    }
-}
-
+// Step metadata (kIMeta bytes): int4 {cnt, imports needed, 0, 0}, then per row
+// slot b < kIB int4 {block row I, own ring slot, dependency slot 0, dependency
+// slot 1} (slots in doubles; missing dependency -> the zero slot).
 template <bool kFwd>
-__global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict__ prog, const int2* __restrict__ gch,
-                                                          const int* __restrict__ imp, const int2* __restrict__ gimp,
-                                                          const double* __restrict__ val,
-                                                          const double* __restrict__ dinv,
-                                                          const double* __restrict__ rhs,
-                                                          const double* __restrict__ zero, double* y, int W,
-                                                          long long* stats) {
+__global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const int4* __restrict__ meta, const char* __restrict__ data,
+                                                          const int2* __restrict__ gst, const long long* __restrict__ gdoff,
+                                                          const int* __restrict__ scnt, const int* __restrict__ imp,
+                                                          const int2* __restrict__ gimp, double* y, int W) {
     extern __shared__ __align__(128) unsigned char sm[];
-    char* ring = reinterpret_cast<char*>(sm);                             // program chunks
-    double* blk = reinterpret_cast<double*>(sm + kINS * kLsCH);           // prefetched blocks
-    uint64_t* full = reinterpret_cast<uint64_t*>(blk + kIP * kIBlk);
+    char* ring = reinterpret_cast<char*>(sm);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kINS * kISlot);
     uint64_t* empty = full + kINS;
-    uint64_t* slotbar = empty + kINS;                                     // prefetch slots (cp.async arrivals)
-    int* imported = reinterpret_cast<int*>(slotbar + kIP);
-    volatile int* cons = imported + 1;                                   // consumer's current need
-    double* xs = reinterpret_cast<double*>(imported + 4);                 // 8W ring | zero 8 | trash 8 | halo ring
+    int* imported = reinterpret_cast<int*>(empty + kINS);
+    volatile int* cons = imported + 1;  // consumer's current import need (importer back-pressure)
+    double* xs = reinterpret_cast<double*>(imported + 4);  // 8W ring | zero 8 | trash 8 | halo ring 8 kIH
     const int g = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int2 ch = gch[g];  // first chunk, steps
-    const int nsteps = ch.y, nchunks = (nsteps + kISPC - 1) / kISPC;
+    const int2 gs = gst[g];  // first step, step count
     if (threadIdx.x == 0) {
         for (int s = 0; s < kINS; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
         }
-        for (int s = 0; s < kIP; ++s) mbar_init(slotbar + s, 1);
         *imported = 0;
         *cons = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = threadIdx.x; i < 16; i += blockDim.x) xs[8 * W + i] = 0.0;
     __syncthreads();
-    if (warp == 2) {  // loader: program chunks -> shared-memory ring
-        if (lane == 0)
-            for (int c = 0; c < nchunks; ++c) {
-                const int s = c & (kINS - 1);
-                if (c >= kINS) mbar_wait(empty + s, ((c / kINS) - 1) & 1);
-                mbar_expect_tx(full + s, kIChunk);
-                bulk_g2s(ring + s * kLsCH, prog + (int64_t)(ch.x + c) * kIChunk, kIChunk, full + s);
+    if (warp == kICW) {  // loader: one bulk copy for the metadata, one for the data of a step
+        if (lane == 0) {
+            long long off = gdoff[g];
+            for (int s = 0; s < gs.y; ++s) {
+                const int slot = s % kINS;
+                if (s >= kINS) mbar_wait(empty + slot, ((s / kINS) - 1) & 1);
+                const int cnt = __ldg(scnt + gs.x + s);
+                mbar_expect_tx(full + slot, kIMeta + cnt * kIRec * 8);
+                bulk_g2s(ring + slot * kISlot, meta + int64_t(gs.x + s) * (kIMeta / 16), kIMeta, full + slot);
+                bulk_g2s(ring + slot * kISlot + kIMeta, data + off, cnt * kIRec * 8, full + slot);
+                off += int64_t(cnt) * kIRec * 8;
             }
+        }
         return;
     }
-    if (warp == 1) {  // importer: previous group's block rows (8 values each), in production order
+    if (warp == kICW + 1) {  // importer: previous group's block rows (8 values each), in production order
         const int2 gi = gimp[g];
         const int* rows = imp + gi.x;
         const int nimp = gi.y;
@@ -152,8 +125,8 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
         const int e = lane >> 3, r = lane & 7;
         int base = 0;
         while (base < nimp) {
-            // ring back-pressure: entry idx overwrites idx - kIH, which is dead once
-            // the consumer's need passed idx - kIH / 2 (checked at setup)
+            // ring back-pressure: entry idx overwrites idx - kIH, dead once the
+            // consumer's need passed idx - kIH / 2 (checked at setup)
             while (base + 4 > *cons + kIH / 2) {
             }
             const int idx = base + e;
@@ -177,33 +150,18 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
         }
         return;
     }
-    // compute warp
-    if (nsteps == 0) return;
-    long long t_start = 0, t_imp = 0, t_blk = 0;
-    if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    const int b = lane >> 3, r = lane & 7;
+    // compute warps: warp w handles row slots 4w .. 4w+3 of every step
+    const int b = warp * 4 + (lane >> 3), r = lane & 7;
     const unsigned imp_a = smem_u32(imported);
     const volatile double* vxs = xs;
     int have = 0;
-    auto rec_of = [&](int s) {
-        return reinterpret_cast<const int*>(ring + ((s / kISPC) & (kINS - 1)) * kLsCH + (s % kISPC) * kIStep);
-    };
-    // prologue: steps 0 .. P-1 (program chunk 0 first)
-    mbar_wait(full, 0);
-    for (int s = 0; s < kIP; ++s) {
-        if (s < nsteps) {
-            if (s > 0 && s % kISPC == 0) mbar_wait(full + ((s / kISPC) & (kINS - 1)), ((s / kISPC) / kINS) & 1);
-            il_prefetch(rec_of(s), lane, val, dinv, rhs, zero, blk + (s % kIP) * kIBlk, slotbar + s % kIP);
-        }
-    }
-    for (int s = 0; s < nsteps; ++s) {
-        const int* rec = rec_of(s);
-        const int cnt = rec[0], need = rec[1];
-        const int* br = rec + 4 + 6 * min(b, cnt - 1);
-        const int I = br[0], myoff = br[1], off0 = br[4], off1 = br[5];
-        if (lane == 0) *cons = need;
-        long long ta = 0, tb = 0, tc = 0;
-        if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
+    for (int s = 0; s < gs.y; ++s) {
+        const int slot = s % kINS;
+        mbar_wait(full + slot, (s / kINS) & 1);
+        const char* st = ring + slot * kISlot;
+        const int4 h = *reinterpret_cast<const int4*>(st);
+        const int cnt = h.x, need = h.y;
+        if (warp == 0 && lane == 0) *cons = need;
         asm volatile(
             "{\n .reg .pred p;\n .reg .s32 r;\n"
             " setp.le.s32 p, %2, %0;\n"
@@ -214,78 +172,88 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const char* __restrict_
             : "+r"(have)
             : "r"(imp_a), "r"(need)
             : "memory");
-        if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb));
-        mbar_wait(slotbar + s % kIP, (s / kIP) & 1);
-        if (stats) {
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tc));
-            t_imp += tb - ta;
-            t_blk += tc - tb;
-        }
-        const double* sb = blk + (s % kIP) * kIBlk + b * 200;
-        double acc = 0.0;
+        const bool act = b < cnt;
+        const int4 mr = *reinterpret_cast<const int4*>(st + 16 + 16 * min(b, cnt - 1));
+        const double* rec = reinterpret_cast<const double*>(st + kIMeta) + min(b, cnt - 1) * kIRec;
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc += sb[c * 8 + r] * vxs[off0 + c] + sb[64 + c * 8 + r] * vxs[off1 + c];
-        const double v = sb[192 + r] - acc;
+        for (int c = 0; c < 8; ++c) {
+            a0 = fma(rec[c * 8 + r], vxs[mr.z + c], a0);
+            a1 = fma(rec[64 + c * 8 + r], vxs[mr.w + c], a1);
+        }
+        const double v = rec[192 + r] - (a0 + a1);
         double vc[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) vc[c] = __shfl_sync(0xffffffffu, v, (lane & ~7) + c);
         double out = kFwd ? v : 0.0;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-            if (kFwd ? (c < r) : (c >= r)) out += sb[128 + c * 8 + r] * vc[c];
-        const bool act = b < cnt;
-        asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(xs + (act ? myoff + r : 8 * W + 8 + r))),
+            if (kFwd ? (c < r) : (c >= r)) out = fma(rec[128 + c * 8 + r], vc[c], out);
+        asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(xs + (act ? mr.y + r : 8 * W + 8 + r))),
                      "d"(out)
                      : "memory");
-        const int64_t yo = act ? int64_t(I) * 8 + r : -1;
+        const int64_t yo = act ? int64_t(mr.x) * 8 + r : -1;
         asm volatile(
             "{\n .reg .pred p;\n setp.ge.s64 p, %2, 0;\n @p st.relaxed.gpu.global.b64 [%0], %1;\n}" ::"l"(y + yo),
             "l"(__double_as_longlong(out)), "l"(yo)
             : "memory");
-        __syncwarp();
-        // release a program chunk once its last step is consumed AND prefetched past
-        if (s % kISPC == kISPC - 1 && lane == 0) mbar_arrive(empty + ((s / kISPC) & (kINS - 1)));
-        // prefetch step s + P (its program chunk may be the next one)
-        const int sp = s + kIP;
-        long long td = 0, te = 0;
-        if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(td));
-        if (sp < nsteps) {
-            if (sp % kISPC == 0) mbar_wait(full + ((sp / kISPC) & (kINS - 1)), ((sp / kISPC) / kINS) & 1);
-            il_prefetch(rec_of(sp), lane, val, dinv, rhs, zero, blk + (sp % kIP) * kIBlk, slotbar + sp % kIP);
-        }
-        if (stats) {
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
-            t_imp += (te - td) << 32;  // prefetch issue time in the high word
-        }
+        // the step's rows are read by the next steps of all four warps; the slot is
+        // free once every warp is past it
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kICW) : "memory");
+        if (warp == 0 && lane == 0) mbar_arrive(empty + slot);
     }
-    if (stats && lane == 0) {
-        long long t_end;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        stats[4 * g] = t_start;
-        stats[4 * g + 1] = t_end;
-        stats[4 * g + 2] = t_imp;
-        stats[4 * g + 3] = t_blk;
+}
+
+// per factorisation: row records (B0, B1, packed inverse) into the stream
+__global__ void k_il_fill(int nc, const long long* __restrict__ roff, const int2* __restrict__ kdep,
+                          const double* __restrict__ val, const double* __restrict__ dinv, char* data) {
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int I = int(t >> 5), lane = int(t & 31);
+    if (I >= nc) return;
+    double* rec = reinterpret_cast<double*>(data + roff[I]);
+    const int2 k = kdep[I];
+    for (int e = lane; e < 192; e += 32) {
+        double v;
+        if (e < 64)
+            v = k.x >= 0 ? val[int64_t(k.x) * 64 + e] : 0.0;
+        else if (e < 128)
+            v = k.y >= 0 ? val[int64_t(k.y) * 64 + e - 64] : 0.0;
+        else
+            v = dinv[int64_t(I) * 64 + e - 128];
+        rec[e] = v;
     }
+}
+
+// per apply: right-hand side into the row records
+__global__ void k_il_rhs(int nc, const long long* __restrict__ roff, const double* __restrict__ rhs, char* data) {
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int I = int(t >> 3), r = int(t & 7);
+    if (I >= nc) return;
+    reinterpret_cast<double*>(data + roff[I])[192 + r] = rhs[int64_t(I) * 8 + r];
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------- setup ------
-// Programs of both directions for the block pattern `pat` (levels from its
-// Kahn schedules).  Returns false when the pattern does not fit the scheme
-// (a block row with more than 2 dependency blocks in one direction, a dependency
-// beyond the previous group, or shared memory).
+// Programs of one direction for the block pattern (levels from its Kahn
+// schedules).  Fails (ok = false) when the pattern does not fit the scheme: a
+// block row with more than 2 dependency blocks in one direction, a dependency
+// beyond the previous group, a halo entry read too far behind the import front,
+// or shared memory.
 struct IlBuilt {
     bool ok = false;
-    int K = 0, W = 0, hmax = 0, nsteps = 0, nchunks = 0;
-    std::vector<char> prog;
-    std::vector<int2> gch, gimp;
+    int K = 0, W = 0, hmax = 0, nsteps = 0;
+    std::vector<int4> meta;        // nsteps x kIMeta / 16
+    std::vector<int> scnt;         // rows per step
+    std::vector<int2> gst, gimp;   // per group: (first step, steps), (import offset, count)
+    std::vector<long long> gdoff;  // per group: data byte offset
     std::vector<int> imp;
+    std::vector<long long> roff;   // per block row: byte offset of its record
+    std::vector<int2> kdep;        // per block row: BSR indices of its dependency blocks (-1: none)
+    int64_t data_bytes = 0;
 };
 
-static int il_smem(int W, int hmax) {
-    return kINS * kLsCH + kIP * kIBlk * 8 + (2 * kINS + kIP) * 8 + 16 + (8 * W + 16 + 8 * std::min(hmax, kIH)) * 8;
-}
+static int il_smem(int W) { return kINS * kISlot + 2 * kINS * 8 + 16 + (8 * W + 16 + 8 * kIH) * 8; }
 
 static void il_build(const std::vector<int>& rp, const std::vector<int>& ci, const std::vector<int>& lev, int n,
                      int dir, int K, IlBuilt& out) {
@@ -298,12 +266,15 @@ static void il_build(const std::vector<int>& rp, const std::vector<int>& ci, con
     for (int g = 0; g <= K; ++g) gstart[g] = int((int64_t)g * n / K);
     for (int g = 0; g < K; ++g)
         for (int t = gstart[g]; t < gstart[g + 1]; ++t) gid[row_of_t(t)] = g;
+    out.kdep.assign(n, make_int2(-1, -1));
     for (int i = 0; i < n; ++i) {
         int d = 0;
         for (int k = rp[i]; k < rp[i + 1]; ++k) {
             const int j = ci[k];
             if (!is_dep(i, j)) continue;
-            if (++d > 2) return;
+            if (d >= 2) return;
+            (d == 0 ? out.kdep[i].x : out.kdep[i].y) = k;
+            ++d;
             if (gid[j] != gid[i] && gid[j] != gid[i] - 1) return;
         }
     }
@@ -342,60 +313,46 @@ static void il_build(const std::vector<int>& rp, const std::vector<int>& ci, con
     gimp_off[K] = int(imp.size());
     int W = 16;
     while (W < maxdist + kIB + 4) W <<= 1;
-    if (il_smem(W, hmax) > 225 * 1024) return;
-    std::vector<int2> gch(K);
-    std::vector<std::vector<int>> steps(K);
-    int64_t nchunks = 0, nsteps = 0;
+    if (il_smem(W) > 225 * 1024) return;
+    const int zero_slot = 8 * W, trash_slot = 8 * W + 8, halo_slot = 8 * W + 16;
+    out.roff.assign(n, 0);
+    out.gst.resize(K);
+    out.gdoff.resize(K);
+    int64_t doff = 0;
     for (int g = 0; g < K; ++g) {
         const int m = gstart[g + 1] - gstart[g];
         const int* q = seq.data() + gstart[g];
-        auto& st = steps[g];
+        out.gst[g] = make_int2(int(out.scnt.size()), 0);
+        out.gdoff[g] = doff;
+        int run_need = 0;
         for (int u = 0; u < m;) {
-            st.push_back(u);
             int cnt = 0;
             while (u + cnt < m && cnt < kIB && lev[q[u + cnt]] == lev[q[u]]) ++cnt;
-            u += cnt;
-        }
-        st.push_back(m);
-        const int ns = int(st.size()) - 1;
-        gch[g] = make_int2(int(nchunks), ns);
-        nchunks += (ns + kISPC - 1) / kISPC;
-        nsteps += ns;
-    }
-    std::vector<char> prog(size_t(nchunks) * kIChunk, 0);
-    const int zero_off = 8 * W, halo_off = 8 * W + 16;
-    for (int g = 0; g < K; ++g) {
-        const int* q = seq.data() + gstart[g];
-        const auto& st = steps[g];
-        int run_need = 0;
-        for (int k = 0; k + 1 < int(st.size()); ++k) {
-            int* rec = reinterpret_cast<int*>(prog.data() + int64_t(gch[g].x + k / kISPC) * kIChunk +
-                                              int64_t(k % kISPC) * kIStep);
-            const int cnt = st[k + 1] - st[k];
+            const size_t mb = out.meta.size();
+            out.meta.resize(mb + kIMeta / 16, make_int4(0, 0, 0, 0));
+            int4* mt = out.meta.data() + mb;
             int need = 0, minneed = 1 << 30;
-            rec[0] = cnt;
             for (int bb = 0; bb < kIB; ++bb) {
-                int* br = rec + 4 + 6 * bb;
-                br[0] = q[st[k]];
-                br[1] = 8 * W + 8;
-                br[2] = br[3] = -1;
-                br[4] = br[5] = zero_off;
+                int4& br = mt[1 + bb];
+                br = make_int4(q[u], trash_slot, zero_slot, zero_slot);
                 if (bb >= cnt) continue;
-                const int i = q[st[k] + bb];
-                br[0] = i;
-                br[1] = 8 * (pos[i] & (W - 1));
+                const int i = q[u + bb];
+                br.x = i;
+                br.y = 8 * (pos[i] & (W - 1));
+                out.roff[i] = doff + int64_t(bb) * kIRec * 8;
                 int d = 0;
                 for (int kk = rp[i]; kk < rp[i + 1]; ++kk) {
                     const int j = ci[kk];
                     if (!is_dep(i, j)) continue;
-                    br[2 + d] = kk;
+                    int sl;
                     if (gid[j] == g) {
-                        br[4 + d] = 8 * (pos[j] & (W - 1));
+                        sl = 8 * (pos[j] & (W - 1));
                     } else {
-                        br[4 + d] = halo_off + 8 * (hidx[j] & (kIH - 1));
+                        sl = halo_slot + 8 * (hidx[j] & (kIH - 1));
                         need = std::max(need, hidx[j] + 1);
                         minneed = std::min(minneed, hidx[j]);
                     }
+                    (d == 0 ? br.z : br.w) = sl;
                     ++d;
                 }
             }
@@ -403,35 +360,42 @@ static void il_build(const std::vector<int>& rp, const std::vector<int>& ci, con
             // entry a step reads must still be in the halo ring
             need = std::max(need, run_need);
             run_need = need;
-            rec[1] = need;
+            mt[0] = make_int4(cnt, need, 0, 0);
             if (minneed != (1 << 30) && need - minneed > kIH / 4) return;
+            out.scnt.push_back(cnt);
+            doff += int64_t(cnt) * kIRec * 8;
+            u += cnt;
         }
+        out.gst[g].y = int(out.scnt.size()) - out.gst[g].x;
     }
-    std::vector<int2> gimp(K);
-    for (int g = 0; g < K; ++g) gimp[g] = make_int2(gimp_off[g], gimp_off[g + 1] - gimp_off[g]);
-    out.prog = std::move(prog);
-    out.gch = std::move(gch);
-    out.gimp = std::move(gimp);
+    out.gimp.resize(K);
+    for (int g = 0; g < K; ++g) out.gimp[g] = make_int2(gimp_off[g], gimp_off[g + 1] - gimp_off[g]);
     out.imp = std::move(imp);
     out.K = K;
     out.W = W;
     out.hmax = hmax;
-    out.nsteps = int(nsteps);
-    out.nchunks = int(nchunks);
+    out.nsteps = int(out.scnt.size());
+    out.data_bytes = doff;
     out.ok = true;
 }
 
 static void il_upload(Ctx& c, IlBuilt& b, IluLs& s) {
-    s.prog.upload(b.prog.data(), b.prog.size(), c.s);
-    s.gch.upload(b.gch.data(), b.K, c.s);
+    s.meta.upload(b.meta.data(), b.meta.size(), c.s);
+    s.scnt.upload(b.scnt.data(), b.scnt.size(), c.s);
+    s.gst.upload(b.gst.data(), b.K, c.s);
+    s.gdoff.upload(b.gdoff.data(), b.K, c.s);
     s.imp.alloc(std::max<size_t>(b.imp.size(), 1));
     if (!b.imp.empty()) s.imp.upload(b.imp.data(), b.imp.size(), c.s);
     s.gimp.upload(b.gimp.data(), b.K, c.s);
+    s.roff.upload(b.roff.data(), b.roff.size(), c.s);
+    s.kdep.upload(b.kdep.data(), b.kdep.size(), c.s);
+    s.data.alloc(size_t(b.data_bytes));
     s.K = b.K;
     s.W = b.W;
     s.hmax = b.hmax;
     s.nsteps = b.nsteps;
-    s.smem = il_smem(b.W, b.hmax);
+    s.nc = int(b.roff.size());
+    s.smem = il_smem(b.W);
     s.ok = true;
 }
 
@@ -452,14 +416,19 @@ bool build_ilu_ls(Ctx& c, Pattern& pat, int K, IluLs& fwd, IluLs& bwd) {
     if (!bf.ok || !bb.ok) return false;
     il_upload(c, bf, fwd);
     il_upload(c, bb, bwd);
-    fwd.zero.alloc(64);
-    MG_CUDA(cudaMemsetAsync(fwd.zero.p, 0, 64 * sizeof(double), c.s));
     c.sync();
     return true;
 }
 
-void ilu_ls_solve(Ctx& c, const IluLs& s, const IluLs& zero_owner, bool fwd, const double* val, const double* dinv,
-                  const double* rhs, double* y) {
+// (Re)fill the solve streams from the factor and the packed inverses.
+void ilu_ls_fill(Ctx& c, IluLs& s, const double* val, const double* dinv) {
+    const int64_t threads = int64_t(s.nc) * 32;
+    k_il_fill<<<int((threads + 255) / 256), 256, 0, c.s>>>(s.nc, s.roff.p, s.kdep.p, val, dinv, s.data.p);
+    check_launch("ilu ls fill");
+    s.filled = true;
+}
+
+void ilu_ls_solve(Ctx& c, IluLs& s, bool fwd, const double* rhs, double* y) {
     static bool attr[2] = {false, false};
     if (!attr[fwd]) {
         if (fwd)
@@ -468,27 +437,16 @@ void ilu_ls_solve(Ctx& c, const IluLs& s, const IluLs& zero_owner, bool fwd, con
             MG_CUDA(cudaFuncSetAttribute(k_ilu_ls<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
         attr[fwd] = true;
     }
-    static const bool want_stats = getenv("MPREC_ILU_LS_STATS") != nullptr;
-    DBuf<long long> st;
-    if (want_stats) st.alloc(4 * s.K);
+    if (!s.filled) throw Error(MPREC_SETUP, "ilu ls: stream not filled");
+    k_il_rhs<<<int((int64_t(s.nc) * 8 + 255) / 256), 256, 0, c.s>>>(s.nc, s.roff.p, rhs, s.data.p);
+    check_launch("ilu ls rhs");
     if (fwd)
-        k_ilu_ls<true><<<s.K, kIThreads, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, val, dinv, rhs,
-                                                        zero_owner.zero.p, y, s.W, st.p);
+        k_ilu_ls<true><<<s.K, kIThreads, s.smem, c.s>>>(s.meta.p, s.data.p, s.gst.p, s.gdoff.p, s.scnt.p, s.imp.p,
+                                                        s.gimp.p, y, s.W);
     else
-        k_ilu_ls<false><<<s.K, kIThreads, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, val, dinv, rhs,
-                                                         zero_owner.zero.p, y, s.W, st.p);
+        k_ilu_ls<false><<<s.K, kIThreads, s.smem, c.s>>>(s.meta.p, s.data.p, s.gst.p, s.gdoff.p, s.scnt.p, s.imp.p,
+                                                         s.gimp.p, y, s.W);
     check_launch(fwd ? "ilu ls fwd" : "ilu ls bwd");
-    if (want_stats) {
-        auto h = st.to_host(c.s);
-        long long t0 = h[0];
-        for (int g = 0; g < s.K; ++g) t0 = std::min(t0, h[4 * g]);
-        fprintf(stderr, "[ilu ls %s] K=%d steps=%d (group: start end import_wait_us block_wait_us)\n", fwd ? "fwd" : "bwd",
-                s.K, s.nsteps);
-        for (int g = 0; g < s.K; g += std::max(1, s.K / 10))
-            fprintf(stderr, "  g%3d %9.1f %9.1f import %9.1f prefetch-issue %9.1f block %9.1f\n", g,
-                    (h[4 * g] - t0) * 1e-3, (h[4 * g + 1] - t0) * 1e-3, (h[4 * g + 2] & 0xffffffffll) * 1e-3,
-                    (h[4 * g + 2] >> 32) * 1e-3, h[4 * g + 3] * 1e-3);
-    }
 }
 
 }  // namespace mg

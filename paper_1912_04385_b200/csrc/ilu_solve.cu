@@ -225,15 +225,23 @@ void Ilu::factor(Ctx& c) {
         dinv.ensure((size_t)lu.nc * 64);
         k_ilu_dinv8<<<(lu.nc + 127) / 128, 128, 0, c.s>>>(lu.dpos, lu.val, lu.nc, dinv.p);
         check_launch("ilu dinv");
-        // level-synchronous solve programs (ilu_ls.cu), opt-in: MPREC_ILU_LS=<groups>.
-        // Measured slower than the warp-per-block-row kernel at c5 (28 vs 5.7 ms per
-        // sweep: each step needs 6.4 KB of factor blocks and the prefetch ring that
-        // fits next to the 128 KB halo does not cover the HBM latency), DESIGN.md §5.1
+        // level-synchronous solve streams (ilu_ls.cu) when the pattern fits them
+        // (<= 2 dependency blocks per direction, dependencies within the previous
+        // group): MPREC_ILU_LS=<groups> (default 148; 0 = warp-per-block-row kernel)
         const int ls_k = [] {  // read per factorisation (tests toggle it)
             const char* e = getenv("MPREC_ILU_LS");
-            return e ? atoi(e) : 0;
+            return e ? atoi(e) : 148;
         }();
-        if (ls_k > 0 && pat && !ls_fwd.ok) build_ilu_ls(c, *pat, std::min(ls_k, c.sm_count), ls_fwd, ls_bwd);
+        if (ls_k > 0 && pat && lu.nc >= 4096) {
+            if (!ls_fwd.ok) build_ilu_ls(c, *pat, std::min(ls_k, c.sm_count), ls_fwd, ls_bwd);
+            if (ls_fwd.ok && ls_bwd.ok) {
+                ilu_ls_fill(c, ls_fwd, lu.val, dinv.p);
+                ilu_ls_fill(c, ls_bwd, lu.val, dinv.p);
+            }
+        } else {
+            ls_fwd = IluLs();
+            ls_bwd = IluLs();
+        }
     }
 }
 
@@ -254,13 +262,15 @@ void Ilu::apply(Ctx& c, const double* r, double* y) {
     const double bytes = lower_blocks * (8.0 * nb2 + 4.0) + 4.0 * (lu.nc + 1) + 16.0 * nn;
     if (lu.nb > 32) throw Error(MPREC_DIMENSION, "nb > 32 not supported by the ILU solve");
     if (lu.nb == 8 && ls_fwd.ok && ls_bwd.ok) {
+        // algorithmic bytes as for the BSR kernels (factor blocks + vectors); the
+        // stream copy of the right-hand side is charged inside the same scope
         {
             Ctx::Scope sc(&c, MPREC_K_ILU_FWD, bytes);
-            ilu_ls_solve(c, ls_fwd, ls_fwd, true, lu.val, dinv.p, r, ybuf.p);
+            ilu_ls_solve(c, ls_fwd, true, r, ybuf.p);
         }
         {
             Ctx::Scope sc(&c, MPREC_K_ILU_BWD, bytes);
-            ilu_ls_solve(c, ls_bwd, ls_fwd, false, lu.val, dinv.p, ybuf.p, y);
+            ilu_ls_solve(c, ls_bwd, false, ybuf.p, y);
         }
         return;
     }

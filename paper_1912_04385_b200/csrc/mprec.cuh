@@ -140,16 +140,20 @@ void extract_pt(Ctx& c, const BsrView& a, int* erp, int* eci, double* ev);
 // ---- ilu.cu ------------------------------------------------------------------
 // Level-synchronous block ILU(0) solve programs (ilu_ls.cu, nb = 8).
 struct IluLs {
-    bool ok = false;
-    int K = 0, W = 0, hmax = 0, nsteps = 0, smem = 0;
-    DBuf<char> prog;
-    DBuf<int2> gch, gimp;
-    DBuf<int> imp;
-    DBuf<double> zero;  // a zero block (missing dependencies)
+    bool ok = false, filled = false;
+    int K = 0, W = 0, hmax = 0, nsteps = 0, smem = 0, nc = 0;
+    DBuf<int4> meta;            // per step: header + row metadata (ilu_ls.cu)
+    DBuf<int> scnt;             // rows per step
+    DBuf<int2> gst, gimp;       // per group: (first step, steps), (import offset, count)
+    DBuf<long long> gdoff;      // per group: byte offset of its data
+    DBuf<int> imp;              // per group: block rows imported from the previous group
+    DBuf<long long> roff;       // per block row: byte offset of its record in `data`
+    DBuf<int2> kdep;            // per block row: BSR indices of its two dependency blocks
+    DBuf<char> data;            // the solve stream: per row B0, B1, packed inverse, rhs
 };
 bool build_ilu_ls(Ctx& c, Pattern& pat, int K, IluLs& fwd, IluLs& bwd);
-void ilu_ls_solve(Ctx& c, const IluLs& s, const IluLs& zero_owner, bool fwd, const double* val, const double* dinv,
-                  const double* rhs, double* y);
+void ilu_ls_fill(Ctx& c, IluLs& s, const double* val, const double* dinv);
+void ilu_ls_solve(Ctx& c, IluLs& s, bool fwd, const double* rhs, double* y);
 
 struct Ilu {
     BsrView lu;           // values owned elsewhere (or by `own`)
