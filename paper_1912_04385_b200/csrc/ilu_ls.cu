@@ -175,20 +175,22 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const int4* __restrict_
         const bool act = b < cnt;
         const int4 mr = *reinterpret_cast<const int4*>(st + 16 + 16 * min(b, cnt - 1));
         const double* rec = reinterpret_cast<const double*>(st + kIMeta) + min(b, cnt - 1) * kIRec;
-        double a0 = 0.0, a1 = 0.0;
+        // four independent FMA chains of 4 (dependency latency, not throughput, bounds a step)
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            a0 = fma(rec[c * 8 + r], vxs[mr.z + c], a0);
-            a1 = fma(rec[64 + c * 8 + r], vxs[mr.w + c], a1);
+            a[c & 1] = fma(rec[c * 8 + r], vxs[mr.z + c], a[c & 1]);
+            a[2 + (c & 1)] = fma(rec[64 + c * 8 + r], vxs[mr.w + c], a[2 + (c & 1)]);
         }
-        const double v = rec[192 + r] - (a0 + a1);
+        const double v = rec[192 + r] - ((a[0] + a[1]) + (a[2] + a[3]));
         double vc[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) vc[c] = __shfl_sync(0xffffffffu, v, (lane & ~7) + c);
-        double out = kFwd ? v : 0.0;
+        double o[4] = {kFwd ? v : 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-            if (kFwd ? (c < r) : (c >= r)) out = fma(rec[128 + c * 8 + r], vc[c], out);
+            if (kFwd ? (c < r) : (c >= r)) o[c & 3] = fma(rec[128 + c * 8 + r], vc[c], o[c & 3]);
+        const double out = (o[0] + o[1]) + (o[2] + o[3]);
         asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(xs + (act ? mr.y + r : 8 * W + 8 + r))),
                      "d"(out)
                      : "memory");

@@ -53,10 +53,13 @@ def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
     assert rel(rg.x, ro.x) < 1e-6
 
 
+@pytest.mark.parametrize("groups", ["32", "148", "0"])
 @pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
-def test_ilu_level_sync_solve(gpu, orc, cfg2, method, monkeypatch):
-    """Opt-in level-synchronous block ILU(0) solve (ilu_ls.cu) against the oracle."""
-    monkeypatch.setenv("MPREC_ILU_LS", "32")
+def test_ilu_level_sync_solve(gpu, orc, cfg2, method, groups, monkeypatch):
+    """Block ILU(0) solves against the oracle: the level-synchronous solve streams
+    (ilu_ls.cu, default; 32 and 148 groups) and the warp-per-block-row kernel
+    (ilu_solve.cu, MPREC_ILU_LS=0)."""
+    monkeypatch.setenv("MPREC_ILU_LS", groups)
     a, b, _ = cfg2
     sg = gpu.system(a).setup(method, b)
     so = orc.system(a).setup(method, b)
