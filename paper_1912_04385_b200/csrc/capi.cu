@@ -177,7 +177,10 @@ GmresOut gmres_dev(Ctx& c, Krylov& kr, int64_t n, const DevOp& A, const DevOp& M
         // Gram row in one pass, (I + L) h = V^T w, w -= V h in a second pass
         // one re-orthogonalisation pass when ||w|| < 0.7 pre_norm (gmres.cpp:44-50), gated on
         // device; its pass A is fused into the first sweep's pass B (gram_orthogonalise)
-        if (gram_fused() && k + 1 <= 512) {  // the fused pass holds <= 512 basis vectors per row in registers
+        // the fused pass holds <= 512 basis vectors per row in registers; below 24
+        // vectors its per-sub-tile synchronisation and 32-wide butterfly cost more
+        // than the separate pass A' (ncu: 0.95 ms vs 0.26 ms at k = 1)
+        if (gram_fused() && k + 1 <= 512 && k >= 24) {
             gram_orthogonalise(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, sc + 1, sc + 2, sc + 3, kr.part.p, gate);
         } else {
             gram_sweep(c, ct, k, w, n, kr.gt.p, ld, kr.pbuf.p, hc, false, k > 0, sc + 1, sc + 2, kr.part.p, nullptr);
