@@ -605,7 +605,9 @@ class ILU0Factor:
 
 
 # ---- the product library ----------------------------------------------------
-GPU_LIB = os.path.join(_HERE, "libmprec_gpu.so")
+# MPREC_LIB=checked: the bounds-checked build (tests/test_checked.py)
+GPU_LIB = os.path.join(_HERE, "libmprec_gpu_checked.so" if os.environ.get("MPREC_LIB") == "checked"
+                       else "libmprec_gpu.so")
 GEN_LIB = os.path.join(_HERE, "libmprec_gen.so")
 _gpu_api = None
 

@@ -62,8 +62,12 @@ def gpu_sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def build_gpu(force=False):
-    out = os.path.join(HERE, "libmprec_gpu.so")
+def build_gpu(force=False, checked=False):
+    """libmprec_gpu.so, or with checked=True libmprec_gpu_checked.so: the same
+    sources with -DMPREC_CHECKED (device-side bounds checks in the sync-free and
+    level-synchronous kernels, MG_DCHECK) -- test infrastructure standing in for
+    compute-sanitizer, which this GPU pool does not allow."""
+    out = os.path.join(HERE, "libmprec_gpu_checked.so" if checked else "libmprec_gpu.so")
     srcs = gpu_sources()
     hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [
         os.path.join(ROOT, "include", "mprec_gpu.h")]
@@ -71,11 +75,13 @@ def build_gpu(force=False):
         return None
     if not (force or _stale(out, srcs + hdrs)):
         return out
-    objdir = os.path.join(HERE, "_obj")
+    objdir = os.path.join(HERE, "_obj_checked" if checked else "_obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
                     "-I", CSRC, "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+    if checked:
+        flags += ["-DMPREC_CHECKED"]
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         if force or _stale(o, [s] + hdrs):
@@ -91,6 +97,7 @@ def build_gpu(force=False):
 def build_all(force=False):
     build_gen(force)
     build_gpu(force)
+    build_gpu(force, checked=True)
     if os.path.exists(os.path.join(ROOT, "oracle", "Makefile")):
         build_oracle(force)
 

@@ -31,6 +31,25 @@ struct Error : std::runtime_error {
             throw ::mg::Error(MPREC_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
+// Device-side bounds checks of the sync-free / level-synchronous kernels, compiled
+// only into the checked build (libmprec_gpu_checked.so, -DMPREC_CHECKED; the
+// pool's compute-sanitizer is unavailable): a failed check prints and traps, the
+// launch then fails with cudaErrorLaunchFailure -> MPREC_CUDA.
+#ifdef MPREC_CHECKED
+#define MG_DCHECK(cond)                                                                         \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("[mprec checked] %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x, #cond);                                                        \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define MG_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 inline void check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw Error(MPREC_CUDA, std::string(what) + ": " + cudaGetErrorString(e));

@@ -294,6 +294,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
                          : "r"(smem_u32(stn)));
             double xv[ND];
 #pragma unroll
+            for (int d = 0; d < ND; ++d) MG_DCHECK(sl[d] >= 0 && sl[d] < trash);
+            MG_DCHECK(h.x >= 1 && h.x <= 32 && h.w >= 16 && h.w <= kLsCH && h.z >= 0 && h.z <= trash - W - 1);
+#pragma unroll
             for (int d = 0; d < ND; ++d) xv[d] = vxs[sl[d]];
             const bool more = k + 1 < nsteps;  // (select, not a branch)
             ls_slots<ND>((more ? stn : st) + 16 + min(lane, (more ? hn.x : h.x) - 1) * RS, sl);
@@ -308,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
             }
             const double x = ls_dot<ND>(e, xv, cc);
             const int row = lane < h.x ? rs.x : -1;
+            MG_DCHECK(lane >= h.x || (rs.y & kLsSlotMask) < W);
             asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(
                              smem_u32(xs + (lane < h.x ? (rs.y & kLsSlotMask) : trash))),
                          "d"(x)
@@ -480,6 +484,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_lsv(const char* __restrict__
             asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(hn.x), "=r"(hn.y), "=r"(hn.z), "=r"(hn.w)
                          : "r"(smem_u32(stn)));
+            MG_DCHECK(s0.x >= 0 && s0.x < trash && s0.y >= 0 && s0.y < trash && s0.z >= 0 && s0.z < trash &&
+                      s0.w >= 0 && s0.w < trash);
+            MG_DCHECK(h.x >= 1 && h.x <= 32 && h.y >= 1 && h.y <= 8 && h.w >= 16 && h.w <= kLsCH);
             const double x0 = vxs[s0.x], x1 = vxs[s0.y], x2 = vxs[s0.z], x3 = vxs[s0.w];
             const bool more = k + 1 < nsteps;
             const int4 s0n = *reinterpret_cast<const int4*>((more ? stn : st) + 16 +

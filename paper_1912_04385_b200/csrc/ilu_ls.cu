@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const int4* __restrict_
             int pre = 0;
             while (pre < 4 && ((m >> (8 * pre)) & 0xffu) == 0xffu) ++pre;
             pre = min(pre, nimp - base);
+            MG_DCHECK(e >= pre || idx < nimp);
             if (e < pre) halo[int64_t(idx & (kIH - 1)) * 8 + r] = __longlong_as_double((long long)raw);
             if (pre > 0) {
                 __syncwarp();
@@ -174,6 +175,9 @@ __global__ void __launch_bounds__(kIThreads, 1) k_ilu_ls(const int4* __restrict_
             : "memory");
         const bool act = b < cnt;
         const int4 mr = *reinterpret_cast<const int4*>(st + 16 + 16 * min(b, cnt - 1));
+        MG_DCHECK(cnt >= 1 && cnt <= kIB && need >= 0);
+        MG_DCHECK(mr.z >= 0 && mr.z <= 8 * W + 16 + 8 * (kIH - 1) && mr.w >= 0 && mr.w <= 8 * W + 16 + 8 * (kIH - 1));
+        MG_DCHECK(mr.y >= 0 && (mr.y < 8 * W || mr.y == 8 * W + 8) && mr.x >= 0);
         const double* rec = reinterpret_cast<const double*>(st + kIMeta) + min(b, cnt - 1) * kIRec;
         // four independent FMA chains of 4 (dependency latency, not throughput, bounds a step)
         double a[4] = {0.0, 0.0, 0.0, 0.0};

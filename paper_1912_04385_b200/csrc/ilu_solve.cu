@@ -46,9 +46,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_ilu8(const int* __restrict__
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= nc) return;
         const int I = __ldg(order + t);
+        MG_DCHECK(I >= 0 && I < nc);
         const int d = dpos[I];
         const int ka = kFwd ? rp[I] : d + 1;
         const int kb = kFwd ? d : rp[I + 1];
+        MG_DCHECK(ka <= kb && (kb - ka) <= 64);
         // row r of the packed inverse diagonal block (strict lower: inv(L_II),
         // upper incl. diagonal: inv(U_II)) -- independent of the chain
         const double* bd = dinv + (int64_t)I * 64;

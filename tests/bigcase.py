@@ -46,7 +46,27 @@ def setup_digests(s) -> dict:
     return out
 
 
-def run_case(api, cid, iters=500, method=None, setup_digest=True, apply_sample=False, perturb_seed=None, log=print):
+def levelset_digests(s) -> dict:
+    """Digests of the level sets of every sequential sweep: the ILU(0) block DAG
+    (ilu0.cpp:48-57) and Gauss-Seidel on every smoothed AMG level (amg.cpp:31-42),
+    both directions, with the depths."""
+    out = {}
+    for d in (1, -1):
+        lv, nl = s.levelsets(d)
+        out[f"ilu/d{d}"] = digest(lv) + f":{nl}"
+    for st in range(s.n_stages() - 1):
+        try:
+            h = s.stage_amg(st)
+        except Exception:  # -direct stage
+            continue
+        for l in range(h.n_levels - 1):
+            for d in (1, -1):
+                lv, nl = h.levelsets(l, d)
+                out[f"s{st}/l{l}/d{d}"] = digest(lv) + f":{nl}"
+    return out
+
+
+def run_case(api, iters=500, method=None, setup_digest=True, apply_sample=False, perturb_seed=None, log=print):
     import time
     method = method or gen.CONFIG_METHODS[cid][-1]
     a, b, xs = gen.generate(cid)

@@ -94,3 +94,28 @@ def test_c5_setup_and_first_iterations(gpu):
     """Config 5 (2000x2000, nb 8, 10 GB of blocks): setup bitwise, applications at
     1e-10, the first 40 iterations inside the oracle's band."""
     _check(gpu, 5, 40)
+
+
+@pytest.mark.parametrize("cid", [4, 5])
+def test_levelsets_c4_c5(gpu, cid):
+    """north_star "level sets bit-exact" at full size: the level sets of every
+    sequential sweep the device schedules (ILU(0) block DAG, Gauss-Seidel on every
+    smoothed level of both hierarchies, both directions) equal the oracle's
+    (tests/golden/levelsets_c45.npz; c5 level 0: 3,999 levels)."""
+    from paper_1912_04385_b200 import gen
+    from tests.bigcase import levelset_digests
+    path = os.path.join(GOLDEN, "levelsets_c45.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"{path} missing: run tests/golden/make_levelset_golden.py")
+    z = np.load(path)
+    want = {k.split("/", 1)[1]: str(z[k]) for k in z.files if k.startswith(f"c{cid}/")}
+    a, b, _ = gen.generate(cid)
+    s = gpu.system(a)
+    a.values = None
+    s.setup(gen.CONFIG_METHODS[cid][-1], b)
+    got = levelset_digests(s)
+    assert set(got) == set(want)
+    bad = [k for k in want if got[k] != want[k]]
+    assert not bad, bad
+    if cid == 5:
+        assert want["ilu/d1"].endswith(":3999")
