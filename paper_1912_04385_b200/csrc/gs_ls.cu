@@ -309,9 +309,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
                 e[d] = q.x;
                 e[d + 1] = q.y;
             }
-            const double x = ls_dot<ND>(e, xv, cc);
+            double x = ls_dot<ND>(e, xv, cc);
+            // lane groups (header .y: pairs << 8 | quads << 16): quads on lanes
+            // [0, 4 nq), pairs on [4 nq, 4 nq + 2 np); the group's other lanes hold
+            // -(sums of further dependencies) with c' = 0
+            if (h.y >> 8) {
+                const int nq = (h.y >> 16) & 0xff, np2 = 4 * nq + 2 * ((h.y >> 8) & 0xff);
+                const double o1 = __shfl_xor_sync(0xffffffffu, x, 1);
+                if (lane < np2) x += o1;
+                if (nq) {
+                    const double o2 = __shfl_xor_sync(0xffffffffu, x, 2);
+                    if (lane < 4 * nq) x += o2;
+                }
+            }
             const int row = lane < h.x ? rs.x : -1;
-            MG_DCHECK(lane >= h.x || (rs.y & kLsSlotMask) < W);
+            MG_DCHECK(lane >= h.x || rs.x < 0 || (rs.y & kLsSlotMask) < W);
             asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(
                              smem_u32(xs + (lane < h.x ? (rs.y & kLsSlotMask) : trash))),
                          "d"(x)
@@ -628,8 +640,34 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
     int cls = 0;
     while (ls_nd(cls) < maxnd) ++cls;
     // variable-width records (k_gs_lsv) for wide levels unless fixed-class forced
-    const bool var = rec_mode == 2 || (rec_mode == 0 && maxnd > kLsVarMin);
+    const bool var0 = rec_mode == 2 || (rec_mode == 0 && maxnd > kLsVarMin);
+    // lane groups: when most rows fit a smaller class (coarse RS levels: 92-95 %
+    // of the rows have <= 8 of up to 15-19 dependencies) the records use that
+    // class and each wider row takes TWO or FOUR lanes (dependencies 0..ND-1,
+    // ND..2ND-1, ..., summed by xor shuffles).  Quads occupy the first lanes of a
+    // step, then pairs, then single rows, so a level still needs one step per 32
+    // lanes; this also replaces the variable-width records on levels whose widest
+    // row has 17-32 dependencies.  MPREC_LS_PAIRS=0: off.
+    static const bool pairs_on = [] {
+        const char* e = getenv("MPREC_LS_PAIRS");
+        return !(e && e[0] == '0');
+    }();
+    bool pair = false;
+    if (pairs_on && rec_mode == 0 && maxnd > 4) {
+        const int cmax = var0 ? 4 : cls;
+        for (int c2 = 1; c2 < cmax && !pair; ++c2) {
+            if (maxnd > 4 * ls_nd(c2)) continue;
+            int wide = 0;
+            for (int i = 0; i < n; ++i) wide += nd[i] > ls_nd(c2) ? 1 : 0;
+            if (wide * 4 < n) {
+                pair = true;
+                cls = c2;
+            }
+        }
+    }
+    const bool var = var0 && !pair;
     if (var) cls = kLsVar;
+    const int trash_slot = W + 1 + hmax;
     std::vector<char> prog;
     std::vector<int2> gch(K);
     std::vector<long long> coff(n);
@@ -650,11 +688,36 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
                     nd4 = n4;
                     ++cnt;
                 }
-            } else {
+            } else if (!pair) {
                 while (u + cnt < m && cnt < 32 && lev[q[u + cnt]] == L && 16 + (cnt + 1) * ls_rs(cls) <= kLsCH - 16)
                     ++cnt;
             }
-            const int RS = var ? ls_rsv(nd4) : ls_rs(cls), ND = var ? 4 * nd4 : ls_nd(cls), bytes = 16 + cnt * RS;
+            // grouped steps: rows of the level in order until 32 lanes (1, 2 or 4 per row)
+            int npair = 0, nquad = 0, lanes = cnt;
+            std::vector<int> lane_row, lane_half;
+            if (pair) {
+                auto lanes_of = [&](int i) { return nd[i] <= ls_nd(cls) ? 1 : nd[i] <= 2 * ls_nd(cls) ? 2 : 4; };
+                lanes = 0;
+                while (u + cnt < m && lev[q[u + cnt]] == L) {
+                    const int nl = lanes_of(q[u + cnt]);
+                    // (quads first, then pairs: both stay aligned without padding)
+                    if (lanes + nl > 32 || 16 + (lanes + nl) * ls_rs(cls) > kLsCH - 16) break;
+                    lanes += nl;
+                    nquad += nl == 4;
+                    npair += nl == 2;
+                    ++cnt;
+                }
+                // lane layout: quads, then pairs, then single rows
+                for (int want : {4, 2, 1})
+                    for (int r = 0; r < cnt; ++r)
+                        if (lanes_of(q[u + r]) == want)
+                            for (int hh = 0; hh < want; ++hh) {
+                                lane_row.push_back(r);
+                                lane_half.push_back(hh);
+                            }
+                lanes = int(lane_row.size());
+            }
+            const int RS = var ? ls_rsv(nd4) : ls_rs(cls), ND = var ? 4 * nd4 : ls_nd(cls), bytes = 16 + lanes * RS;
             if (off + bytes > kLsCH) {
                 cbase = nchunks * int64_t(kLsCH);
                 prog.resize(size_t(cbase + kLsCH), 0);
@@ -663,9 +726,10 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
             }
             char* base = prog.data() + cbase + off;
             int need = 0;
-            for (int r = 0; r < cnt; ++r) {
+            for (int ln = 0; ln < lanes; ++ln) {
+                const int r = pair ? lane_row[ln] : ln, half = pair ? lane_half[ln] : 0;
                 const int i = q[u + r];
-                char* rec = base + 16 + r * RS;
+                char* rec = base + 16 + ln * RS;
                 int* sl0 = reinterpret_cast<int*>(rec);
                 double* cp = reinterpret_cast<double*>(rec + 16);
                 int* rsl = reinterpret_cast<int*>(rec + 24);
@@ -681,17 +745,23 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
                     return ep0[d];
                 };
                 *cp = 0.0;
-                rsl[0] = i;
-                rsl[1] = (pos[i] & (W - 1)) | (exported[i] ? kLsExportBit : 0);
-                coff[i] = (cbase + off + 16 + r * RS + 16) | (exported[i] ? 1 : 0);
+                if (half == 0) {  // first lane of the row's group
+                    rsl[0] = i;
+                    rsl[1] = (pos[i] & (W - 1)) | (exported[i] ? kLsExportBit : 0);
+                    coff[i] = (cbase + off + 16 + ln * RS + 16) | (exported[i] ? 1 : 0);
+                } else {  // further lanes of a pair / quad: c' = 0, no store
+                    rsl[0] = -1;
+                    rsl[1] = trash_slot;
+                }
                 for (int d = 0; d < std::max(ND, 4); ++d) {
                     if (d < ND) coef(d) = 0.0;
                     if (d < 4 || d < ND) slot(d) = W;
                 }
-                int d = 0;
+                int d = 0, dd = 0;
                 for (int k = rp[i]; k < rp[i + 1]; ++k) {
                     const int j = ci[k];
                     if (!is_dep(i, j)) continue;
+                    if (dd++ / ND != half) continue;  // another lane of the row's group
                     coef(d) = v[k] * invd[i];
                     if (gid[j] == g) {
                         slot(d) = pos[j] & (W - 1);
@@ -702,7 +772,7 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
                     ++d;
                 }
             }
-            const int hdr[4] = {cnt, var ? nd4 : cls, need, bytes};
+            const int hdr[4] = {lanes, var ? nd4 : (cls | (npair << 8) | (nquad << 16)), need, bytes};
             std::memcpy(base, hdr, 16);
             *reinterpret_cast<int*>(prog.data() + cbase) += 1;
             off += bytes;
