@@ -78,78 +78,13 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs(const int* __restrict__ rp
     }
 }
 
-// CTA per band of B consecutive rows (doacross).  The band's new
-// iterate lives in shared memory (kPending sentinel), so dependencies inside
-// the band are resolved by an on-SM poll instead of an L2 round trip; rows of
-// the band are claimed by the CTA's warps in global DAG-level order (`border`)
-// and bands are claimed in sweep order, hence deadlock-free.  Row arithmetic
-// is identical to k_gs (warp per row).  Chosen per AMG level by a setup-time
-// measurement (Amg::setup) against the row-per-warp sweep.
-template <int DIR>
-__global__ void __launch_bounds__(1024) k_gs_cta(const int* __restrict__ rp, const int* __restrict__ ci,
-                                                 const double* __restrict__ v, const double* __restrict__ invd,
-                                                 const double* __restrict__ b, const double* __restrict__ xold,
-                                                 double* xnew, const int* __restrict__ border, int n, int B,
-                                                 int nbands, int* counter) {
-    extern __shared__ double xs[];
-    __shared__ int band_sh, claim_sh;
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int t = atomicAdd(counter, 1);
-            band_sh = DIR > 0 ? t : nbands - 1 - t;
-            claim_sh = 0;
-            if (t >= nbands) band_sh = -1;
-        }
-        __syncthreads();
-        const int band = band_sh;
-        if (band < 0) return;
-        const int b0 = band * B, b1 = min(n, b0 + B), nrow = b1 - b0;
-        for (int q = threadIdx.x; q < nrow; q += blockDim.x)
-            reinterpret_cast<unsigned long long*>(xs)[q] = kPending;
-        __syncthreads();
-        for (;;) {
-            int t = 0;
-            if (lane == 0) t = atomicAdd(&claim_sh, 1);
-            t = __shfl_sync(0xffffffffu, t, 0);
-            if (t >= nrow) break;
-            const int i = __ldg(border + b0 + t);
-            const int k0 = __ldg(rp + i), k1 = __ldg(rp + i + 1);
-            const double bi = __ldg(b + i), dii = __ldg(invd + i);
-            double acc = 0.0;
-            for (int base = k0; base < k1; base += 32) {
-                const int k = base + lane;
-                const bool valid = k < k1;
-                const int j = valid ? __ldg(ci + k) : i;
-                const bool off = valid && j != i;
-                const double a = off ? __ldg(v + k) : 0.0;
-                const bool dep = off && (DIR > 0 ? (j < i) : (j > i));
-                const bool local = dep && j >= b0 && j < b1;
-                double xj = 0.0;
-                if (off && !dep && xold) xj = __ldg(xold + j);
-                unsigned long long raw = 0;
-                if (dep && !local) raw = ld_relaxed(xnew + j);
-                if (local) raw = reinterpret_cast<volatile unsigned long long*>(xs)[j - b0];
-                bool pend = dep && raw == kPending;
-                while (__any_sync(0xffffffffu, pend)) {
-                    if (pend) {
-                        raw = local ? reinterpret_cast<volatile unsigned long long*>(xs)[j - b0] : ld_relaxed(xnew + j);
-                        pend = raw == kPending;
-                    }
-                }
-                if (dep) xj = __longlong_as_double((long long)raw);
-                acc += a * xj;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) {
-                const double xi = (bi - acc) * dii;
-                reinterpret_cast<volatile double*>(xs)[i - b0] = xi;
-                st_pub(xnew + i, xi);
-            }
-        }
-    }
+// rows sorted by column with the diagonal present (the LS programs' precondition)
+__global__ void k_sorted(const int* rp, const int* ci, const int* diag, int n, int* bad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    bool ok = diag[i] >= rp[i] && diag[i] < rp[i + 1] && ci[diag[i]] == i;
+    for (int k = rp[i] + 1; k < rp[i + 1]; ++k) ok = ok && ci[k - 1] < ci[k];
+    if (!ok) atomicOr(bad, 1);
 }
 
 __global__ void k_band_key(const int* lev, int n, int B, unsigned long long* key, int* row) {
@@ -237,32 +172,15 @@ void build_band_order(Ctx& c, int n, const int* lev, int B, DBuf<int>& border) {
     c.sync();
 }
 
-void gs_sweep_cta(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
-                  int dir, bool xold_zero, const int* border, int B) {
-    const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 4.0 * a.n + 24.0 * a.n;
-    Ctx::Scope sc(&c, MPREC_K_GS, bytes);
-    int* ctr = c.counters.p + 7;
-    MG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int), c.s));
-    const int nbands = (a.n + B - 1) / B;
-    const size_t smem = size_t(B) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        MG_CUDA(cudaFuncSetAttribute(k_gs_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        MG_CUDA(cudaFuncSetAttribute(k_gs_cta<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
-    static const int threads = [] {
-        const char* e = getenv("MPREC_GS_CTA_THREADS");
-        return e ? atoi(e) : 1024;
-    }();
-    const int grid = std::max(1, std::min(nbands, c.sm_count * std::max(1, 2048 / threads)));
-    if (dir > 0)
-        k_gs_cta<1><<<grid, threads, smem, c.s>>>(a.rp, a.ci, a.v, invd, b, xold_zero ? nullptr : xold, xnew, border, a.n,
-                                              B, nbands, ctr);
-    else
-        k_gs_cta<-1><<<grid, threads, smem, c.s>>>(a.rp, a.ci, a.v, invd, b, xold_zero ? nullptr : xold, xnew, border,
-                                               a.n, B, nbands, ctr);
-    check_launch("gs_sweep_cta");
+bool csr_sorted(Ctx& c, const CsrView& a) {
+    if (a.n == 0) return true;
+    DBuf<int> bad(1);
+    MG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.s));
+    k_sorted<<<(a.n + 255) / 256, 256, 0, c.s>>>(a.rp, a.ci, a.diag, a.n, bad.p);
+    int h = 1;
+    MG_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+    c.sync();
+    return h == 0;
 }
 
 void compute_invd(Ctx& c, const CsrView& a, double* invd) {
@@ -296,21 +214,14 @@ void dense_gemv(Ctx& c, const double* m, int n, const double* x, double* y) {
     check_launch("dense_gemv");
 }
 
-// one Gauss-Seidel direction on level L: band schedule when available
+// one Gauss-Seidel direction on level L with the kernel chosen at setup
 static void level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold, double* xnew, int dir, bool zero) {
-    const BandSched& bs = dir > 0 ? L.band_fwd : L.band_bwd;
     const LsSched& ls = dir > 0 ? L.ls_fwd : L.ls_bwd;
     if (ls.ok)
         gs_sweep_ls(c, L.a, L.invd.p, r, xold, xnew, zero, ls);
-    else if (bs.ok)
-        gs_band_sweep(c, bs, L.a.nnz, L.n, r, zero ? nullptr : xold, xnew);
-    else if (L.seg)
-        gs_sweep_seg(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.seg_fwd : L.seg_bwd);
     else if (L.cl_size > 0)
         gs_sweep_cluster(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.border_f.p : L.border_b.p,
                          L.cl_size, L.cl_R);
-    else if (L.cta_B > 0)
-        gs_sweep_cta(c, L.a, L.invd.p, r, xold, xnew, dir, zero, dir > 0 ? L.border_f.p : L.border_b.p, L.cta_B);
     else
         gs_sweep(c, L.a, r, xold, xnew, dir, zero, dir > 0 ? L.ofwd : L.obwd, L.invd.p);
 }
@@ -353,22 +264,6 @@ void Amg::apply(Ctx& c, const double* r, double* x) { cycle(c, 0, r, x); }
 }  // namespace mg
 
 namespace mg {
-extern long long* g_band_ts;
-// Diagnostics: per-band timeline of one forward band sweep on level l
-void gs_band_timeline(Ctx& c, Amg& amg, int l, long long* host_ts, int* nbands) {
-    AmgLevel& L = *amg.lv[l];
-    if (!L.band_fwd.ok) throw Error(MPREC_SETUP, "no band schedule on this level");
-    DBuf<long long> ts(3 * L.band_fwd.nbands + 2 * L.band_fwd.nchunks);
-    fill(c, L.b.p, 1.0, L.n);
-    fill_pending(c, L.xf.p, L.n);
-    g_band_ts = ts.p;
-    level_sweep(c, L, L.b.p, nullptr, L.xf.p, +1, true);
-    c.sync();
-    g_band_ts = nullptr;
-    ts.download(host_ts, 3 * L.band_fwd.nbands + 2 * L.band_fwd.nchunks, c.s);
-    c.sync();
-    *nbands = L.band_fwd.nbands;
-}
 // Diagnostics: time `reps` forward+backward sweeps on level l of an AMG.
 void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int* nl_f, int* nl_b) {
     AmgLevel& L = *amg.lv[l];
@@ -395,8 +290,8 @@ void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int
     }
     *ms_f = tf / reps;
     *ms_b = tb / reps;
-    *nl_f = L.band_fwd.ok ? -L.band_fwd.nbands : L.own_fwd.nlev;
-    *nl_b = L.band_bwd.ok ? -L.band_bwd.nbands : L.own_bwd.nlev;
+    *nl_f = L.own_fwd.nlev;
+    *nl_b = L.own_bwd.nlev;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
@@ -404,12 +299,18 @@ void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int
 }  // namespace mg
 
 namespace mg {
-// Setup-time choice of the sweep kernel for one level (measure, don't guess):
-// row-per-warp (cross-SM hops), CTA bands of 4096 / 8192 rows (on-SM hops) or
-// band-segment chains (gs_seg.cu) or a whole level in one thread block cluster
-// (gs_cluster.cu).  MPREC_GS_MODE forces one: warp | cta | seg | cluster.
-// LS group counts by level size, in order of preference (B200 measurements,
-// DESIGN.md §5.1); the next one is tried when a program does not fit.
+// Setup-time choice of the sweep kernel for one level.  The kernels round a
+// row's sum in different orders (the LS programs pre-scale by 1/a_ii and sum the
+// previous iterate's part first), so the choice is a fixed rule -- not timing --
+// and setups are bitwise reproducible:
+//   1. the level-synchronous programs (gs_ls.cu) with the first group count of
+//      ls_group_counts(n) that fits (B200 measurements);
+//   2. else the thread-block-cluster sweep (gs_cluster.cu) when the level's
+//      iterate fits one cluster's shared memory;
+//   3. else the warp-per-row sweep in topological claim order (k_gs).
+// MPREC_GS_MODE=warp | cluster | ls forces one (tests; `ls` with MPREC_GS_LS_K
+// groups, default 16, and MPREC_GS_LS_REC=0|1|2 auto / fixed-class / variable-
+// width records).
 static std::vector<int> ls_group_counts(int n) {
     if (n >= (1 << 20)) return {74, 148, 37};
     if (n >= 300000) return {148, 74, 37};
@@ -419,228 +320,44 @@ static std::vector<int> ls_group_counts(int n) {
 }
 
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
-    L.cta_B = 0;
-    L.seg = false;
     L.ls_fwd = LsSched();
     L.ls_bwd = LsSched();
-    std::string force = [] {  // read per setup so tests can force each kernel
+    L.cl_size = 0;
+    const std::string force = [] {  // read per setup so tests can force each kernel
         const char* e = getenv("MPREC_GS_MODE");
         return std::string(e ? e : "");
     }();
-    // The sweep kernels round a row's sum in different orders (the LS program
-    // pre-scales by 1/a_ii and sums the previous iterate's part first), so the
-    // kernel choice must not depend on timing: the default is a fixed rule (the
-    // first LS program that fits, the cluster kernel on levels whose iterate fits
-    // one cluster, else the warp-per-row sweep) and setups are bitwise
-    // reproducible.  MPREC_GS_MODE=tune restores the timed search (experiments).
-    const bool timed = force == "tune";
-    if (timed) force.clear();
-    L.cl_size = 0;
     if (force == "warp") return;
+    const bool have_lev = L.glev_f && L.glev_b;
     if (force == "ls") {
-        if (!L.glev_f || !L.glev_b || !csr_sorted(c, L.a)) return;
+        if (!have_lev || !csr_sorted(c, L.a)) return;
         const int K = [] {
             const char* e = getenv("MPREC_GS_LS_K");
             return e ? atoi(e) : 16;
         }();
         const int rec = [] {
-            const char* e = getenv("MPREC_GS_LS_REC");  // 0 auto, 1 fixed class, 2 variable width
+            const char* e = getenv("MPREC_GS_LS_REC");
             return e ? atoi(e) : 0;
         }();
         build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, rec, L.ls_fwd, L.ls_bwd);
         return;
     }
-    // candidates by size (B200 measurements): the band kernels only
-    // win on the finest, million-row levels; the cluster kernel needs the whole
-    // level's iterate in one cluster's shared memory
-    const bool try_cta = !force.empty() || L.n >= (1 << 20);
-    const bool try_seg = !force.empty() || L.n >= (2 << 20);
+    if (force.empty() && have_lev && L.n >= 512 && csr_sorted(c, L.a))
+        for (int K : ls_group_counts(L.n))
+            if (build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) {
+                if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: level-sync K=%d\n", L.n, K);
+                return;
+            }
     int cl_R = 0;
     const int cl_size = gs_cluster_plan(L.n, &cl_R);
-    const bool try_cl = cl_size > 0 && (force.empty() || force == "cluster");
-    if (force == "cluster") {
-        if (!try_cl) return;
+    if (cl_size > 0 && (force.empty() || force == "cluster")) {
         L.cl_size = cl_size;
         L.cl_R = cl_R;
         build_band_order(c, L.n, sf.level.p, cl_R, L.border_f);
         build_band_order(c, L.n, sb.level.p, cl_R, L.border_b);
+        if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: cluster of %d\n", L.n, cl_size);
         return;
     }
-    const bool try_ls = L.glev_f && L.glev_b && L.n >= 512;
-    if (force.empty() && !timed) {
-        if (try_ls && csr_sorted(c, L.a))
-            for (int K : ls_group_counts(L.n))
-                if (build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) {
-                    if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: level-sync K=%d\n", L.n, K);
-                    return;
-                }
-        if (cl_size > 0) {
-            L.cl_size = cl_size;
-            L.cl_R = cl_R;
-            build_band_order(c, L.n, sf.level.p, cl_R, L.border_f);
-            build_band_order(c, L.n, sb.level.p, cl_R, L.border_b);
-            if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: cluster of %d\n", L.n, cl_size);
-            return;
-        }
-        if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: row-per-warp\n", L.n);
-        return;
-    }
-    // million-row levels: the level-synchronous program beats the band kernels by
-    // 3-4x, so their schedules are not built and timed
-    if (force.empty() && !try_cta && !try_seg && !try_cl && !try_ls) return;
-    const bool sorted = csr_sorted(c, L.a);
-    if (force == "seg") {
-        if (!sorted) return;
-        const int bsz = [] {
-            const char* e = getenv("MPREC_GS_SEG_B");
-            return e ? atoi(e) : 8192;
-        }();
-        build_seg_sched(c, L.a, L.seg_fwd, L.seg_bwd);
-        build_seg_bands(c, L.seg_fwd, bsz);
-        build_seg_bands(c, L.seg_bwd, bsz);
-        L.seg = true;
-        return;
-    }
-    fill(c, L.b.p, 1.0, L.n);
-    cudaEvent_t e0, e1;
-    MG_CUDA(cudaEventCreate(&e0));
-    MG_CUDA(cudaEventCreate(&e1));
-    auto time_fwd = [&]() {
-        float best = 1e30f;
-        for (int rep = 0; rep < 2; ++rep) {
-            fill_pending(c, L.xf.p, L.n);
-            cudaEventRecord(e0, c.s);
-            level_sweep(c, L, L.b.p, nullptr, L.xf.p, +1, true);
-            cudaEventRecord(e1, c.s);
-            cudaEventSynchronize(e1);
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, e0, e1);
-            best = std::min(best, ms);
-        }
-        return best;
-    };
-    const char* names[5] = {"row-per-warp", "cta-band", "band-segment", "cluster", "level-sync"};
-    int best_mode = 0, b_best = 0;
-    // level-synchronous programs (gs_ls.cu) first: on levels above 50k rows they
-    // beat the band kernels by 2-4x, so those are only built and
-    // timed when no LS program fits the level.  Group counts by level size, the
-    // next candidate tried only when a program does not fit (dependency beyond
-    // the previous group, shared memory); both directions built together.
-    int ls_K = 0;
-    LsSched ls_bf, ls_bb;
-    float t_ls = 1e30f;
-    if (try_ls && sorted && force.empty()) {
-        const std::vector<int> cands = ls_group_counts(L.n);
-        const bool first_fit = L.n >= 50000;  // large levels: the first program that fits
-        for (int K : cands) {
-            if (!build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) continue;
-            LsSched keep_b = std::move(L.ls_bwd);
-            L.ls_bwd = LsSched();
-            const float t = time_fwd();
-            if (t < t_ls) {
-                t_ls = t;
-                ls_K = K;
-                ls_bf = std::move(L.ls_fwd);
-                ls_bb = std::move(keep_b);
-            }
-            L.ls_fwd = LsSched();
-            if (first_fit) break;
-        }
-    }
-    const bool skip_band = ls_K > 0 && L.n >= 50000;
-    float t_best = force.empty() ? time_fwd() : 1e30f;
-    if ((force.empty() && try_cta && !skip_band) || force == "cta") {
-        for (int bsz : {4096, 8192}) {
-            if (L.n < 2 * bsz) continue;
-            L.cta_B = bsz;
-            build_band_order(c, L.n, sf.level.p, bsz, L.border_f);
-            const float t = time_fwd();
-            if (t < t_best) {
-                t_best = t;
-                b_best = bsz;
-                best_mode = 1;
-            }
-        }
-        L.cta_B = 0;
-    }
-    int seg_best = 0;
-    if (sorted && ((force.empty() && try_seg && !skip_band) || force == "seg")) {
-        build_seg_sched(c, L.a, L.seg_fwd, L.seg_bwd);
-        L.seg = true;
-        for (int bsz : {4096, 8192}) {
-            build_seg_bands(c, L.seg_fwd, bsz);
-            const float t = time_fwd();
-            if (t < t_best) {
-                t_best = t;
-                best_mode = 2;
-                seg_best = bsz;
-            }
-            if (L.n <= bsz) break;
-        }
-        L.seg = false;
-    }
-    int cl_best = 0, cl_best_R = 0;
-    if (try_cl) {
-        // every feasible cluster size: more CTAs = more warps in flight, fewer local hops
-        for (int want : {1, 2, 4, 8, 16}) {
-            int r = 0;
-            const int cs = gs_cluster_plan(L.n, &r, want);
-            if (cs != want) continue;
-            L.cl_size = cs;
-            L.cl_R = r;
-            build_band_order(c, L.n, sf.level.p, r, L.border_f);
-            float t = 1e30f;
-            try {
-                t = time_fwd();
-            } catch (const Error&) {  // cluster not schedulable on this device
-                cudaGetLastError();
-            }
-            L.cl_size = 0;
-            if (t < t_best) {
-                t_best = t;
-                best_mode = 3;
-                cl_best = cs;
-                cl_best_R = r;
-            }
-        }
-    }
-    // the level-synchronous program when it is the fastest candidate
-    if (ls_K > 0 && t_ls < t_best) {
-        t_best = t_ls;
-        best_mode = 4;
-        L.ls_fwd = std::move(ls_bf);
-        L.ls_bwd = std::move(ls_bb);
-    } else {
-        ls_K = 0;
-        L.ls_fwd = LsSched();
-        L.ls_bwd = LsSched();
-    }
-    if (best_mode != 2) {
-        L.seg_fwd = SegSched();
-        L.seg_bwd = SegSched();
-    }
-    L.seg = best_mode == 2;
-    if (L.seg) {
-        build_seg_bands(c, L.seg_fwd, seg_best);
-        build_seg_bands(c, L.seg_bwd, seg_best);
-    }
-    L.cta_B = best_mode == 1 ? b_best : 0;
-    if (best_mode == 1) {
-        build_band_order(c, L.n, sf.level.p, b_best, L.border_f);
-        build_band_order(c, L.n, sb.level.p, b_best, L.border_b);
-    } else if (best_mode == 3) {
-        L.cl_size = cl_best;
-        L.cl_R = cl_best_R;
-        build_band_order(c, L.n, sf.level.p, cl_best_R, L.border_f);
-        build_band_order(c, L.n, sb.level.p, cl_best_R, L.border_b);
-    } else {
-        L.border_f.release();
-        L.border_b.release();
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (trace_on())
-        fprintf(stderr, "[mprec] level n=%d sweep: %s B=%d (%.3f ms fwd)\n", L.n, names[best_mode],
-                best_mode == 2 ? seg_best : (best_mode == 3 ? L.cl_size : best_mode == 4 ? ls_K : L.cta_B), t_best);
+    if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: row-per-warp\n", L.n);
 }
 }  // namespace mg

@@ -1074,21 +1074,6 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
         finish_helper();
         if (qerr) std::rethrow_exception(qerr);
     }
-    {
-        static const bool band_on = [] {
-            const char* e = getenv("MPREC_GS_BAND");
-            return e && e[0] == '1';  // opt-in
-        }();
-        Trace tr(&c, "amg band schedules");
-        if (band_on)
-            for (size_t li = 0; li + 1 < lv.size(); ++li) {
-                AmgLevel& l = *lv[li];
-                const int* gf = (li == 0 && pat) ? pat->fwd.level.p : l.own_fwd.level.p;
-                const int* gb = (li == 0 && pat) ? pat->bwd.level.p : l.own_bwd.level.p;
-                build_band_sched(c, l.a, +1, gf, l.band_fwd);
-                build_band_sched(c, l.a, -1, gb, l.band_bwd);
-            }
-    }
     for (auto& l : lv) {
         l->x.ensure(std::max(l->n, 1));
         l->b.ensure(std::max(l->n, 1));

@@ -307,8 +307,6 @@ void write_system(const char* mtx, const char* layout, const char* rhs, int nc, 
 void ilu_timeline(Ctx& c, Ilu& ilu, const double* r, double* y, long long* ts_dev, int blocks);
 void gs_bench(Ctx& c, Amg& amg, int l, int reps, double* ms_f, double* ms_b, int* nl_f, int* nl_b);
 void gs_ls_experiment(Ctx& c, Amg& amg, int l, int K, int reps, double* out);
-void gs_seg_timeline(Ctx& c, Amg& amg, int l, long long* host, int* nseg);
-void gs_band_timeline(Ctx& c, Amg& amg, int l, long long* host_ts, int* nbands);
 }
 
 // ============================================================ AMG handle ==
@@ -1209,25 +1207,6 @@ int mprec_gpu_debug_gs_ls(mprec_gpu_system* h, int stage, int level, int K, int 
         Amg* a = (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) ? h->amgT.get() : h->amgP.get();
         if (!a || level < 0 || level + 1 >= a->n_levels()) throw Error(MPREC_INDEX, "level out of range");
         gs_ls_experiment(h->ctx, *a, level, K, reps, out10);
-    });
-}
-
-// diagnostics: per-segment timeline of one forward band-segment sweep (host: 4 * n)
-int mprec_gpu_debug_seg_timeline(mprec_gpu_system* h, int stage, int level, long long* host, int* nseg) {
-    return guard([&] {
-        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
-        Amg* a = (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) ? h->amgT.get() : h->amgP.get();
-        if (!a || level < 0 || level + 1 >= a->n_levels()) throw Error(MPREC_INDEX, "level out of range");
-        gs_seg_timeline(h->ctx, *a, level, host, nseg);
-    });
-}
-
-
-int mprec_gpu_debug_band_timeline(mprec_gpu_system* h, int stage, int level, long long* ts, int* nbands) {
-    return guard([&] {
-        if (!h || !h->ready) throw Error(MPREC_SETUP, "setup not done");
-        Amg* a = (h->method == MPREC_METHOD_CPTR3_AMG && stage == 0) ? h->amgT.get() : h->amgP.get();
-        gs_band_timeline(h->ctx, *a, level, ts, nbands);
     });
 }
 

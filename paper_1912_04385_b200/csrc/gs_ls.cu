@@ -648,7 +648,7 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
     // step, then pairs, then single rows, so a level still needs one step per 32
     // lanes; this also replaces the variable-width records on levels whose widest
     // row has 17-32 dependencies.  MPREC_LS_PAIRS=0: off.
-    static const bool pairs_on = [] {
+    const bool pairs_on = [] {  // read per build (tests toggle it)
         const char* e = getenv("MPREC_LS_PAIRS");
         return !(e && e[0] == '0');
     }();

@@ -38,15 +38,6 @@ struct Sched {
     int n = 0;
     int nlev = 0;
 };
-// Segment-chain sweep schedule (gs_seg.cu): segments [start[s], start[s+1])
-// are dependency chains of <= 32 rows; sched orders the segments.
-struct SegSched {
-    DBuf<int> start;
-    Sched sched;
-    std::vector<int> hstart;        // host copy of start
-    int B = 0, nbands = 0, band_rows = 0;
-    DBuf<int> bord, bseg0, brow0;   // band-local segment order, band -> first segment / first row
-};
 // dir = +1: row i depends on stored k < i; dir = -1: on stored k > i.
 void build_sched(Ctx& c, int n, const int* rp, const int* ci, int dir, Sched& out);
 
@@ -177,21 +168,6 @@ struct AmgParams {
     int max_levels = 25;
 };
 
-// Band ("doacross") schedule of one Gauss-Seidel sweep direction (gs_band.cu).
-struct BandSched {
-    bool ok = false;
-    int B = 0, nbands = 0, nchunks = 0, slot_bytes = 0, rec_max = 0, depth = 0, dir = 0, smem = 0, nlev_total = 0;
-    DBuf<int4> chunks;
-    DBuf<long long> coff;
-    DBuf<int> band_chunk, band_recb;
-    DBuf<unsigned char> rec;
-};
-// `glev`: global DAG levels of the same direction (sched.cu); rows of a band are
-// processed in global-level order so consecutive bands advance in lockstep.
-bool build_band_sched(Ctx& c, const CsrView& a, int dir, const int* glev, BandSched& s);
-void gs_band_sweep(Ctx& c, const BandSched& s, int64_t nnz, int n, const double* b, const double* xold,
-                   double* xnew);
-
 // Level-synchronous pipelined sweep schedule (gs_ls.cu): K groups of
 // consecutive rows, each a stream of program chunks processed by one warp.
 constexpr int kLsCH = 16384;  // program chunk bytes
@@ -231,13 +207,9 @@ struct AmgLevel {
     Sched own_fwd, own_bwd;           // Gauss-Seidel claim orders
     const int* ofwd = nullptr;        // (level 0 may borrow the block pattern's)
     const int* obwd = nullptr;
-    BandSched band_fwd, band_bwd;     // band schedules (opt-in, MPREC_GS_BAND=1)
     DBuf<double> invd;                // 1 / a_ii
-    int cta_B = 0;                    // CTA-band sweep: rows per band (0: row-per-warp sweep)
-    DBuf<int> border_f, border_b;     // band rows in global level order (fwd / bwd)
+    DBuf<int> border_f, border_b;     // cluster sweep: rows per CTA band in global level order
     int cl_size = 0, cl_R = 0;        // cluster sweep (gs_cluster.cu): CTAs, rows per CTA
-    bool seg = false;                 // segment-chain sweep (gs_seg.cu)
-    SegSched seg_fwd, seg_bwd;        // segment bounds + claim orders (fwd / bwd)
 };
 
 struct Amg {
@@ -268,13 +240,9 @@ void dense_gemv(Ctx& c, const double* m_rowmajor, int n, const double* x, double
 void compute_invd(Ctx& c, const CsrView& a, double* invd);
 void build_band_order(Ctx& c, int n, const int* lev, int B, DBuf<int>& border);
 bool csr_sorted(Ctx& c, const CsrView& a);
-void build_seg_sched(Ctx& c, const CsrView& a, SegSched& fwd, SegSched& bwd);
-void build_seg_bands(Ctx& c, SegSched& seg, int B);
 int gs_cluster_plan(int n, int* rows_per_cta, int min_cs = 1);
 void gs_sweep_cluster(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
                       int dir, bool xold_zero, const int* border, int csize, int R);
-void gs_sweep_seg(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
-                  int dir, bool xold_zero, const SegSched& seg);
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb);
 
 }  // namespace mg

@@ -66,7 +66,7 @@ def levelset_digests(s) -> dict:
     return out
 
 
-def run_case(api, iters=500, method=None, setup_digest=True, apply_sample=False, perturb_seed=None, log=print):
+def run_case(api, cid, iters=500, method=None, setup_digest=True, apply_sample=False, perturb_seed=None, log=print):
     import time
     method = method or gen.CONFIG_METHODS[cid][-1]
     a, b, xs = gen.generate(cid)

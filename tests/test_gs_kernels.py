@@ -1,11 +1,12 @@
 """Every Gauss-Seidel sweep kernel against the oracle.
 
-The setup-time autotuner (amg_cycle.cu: tune_level_sweep) picks, per AMG
-level, the fastest of the dependency-scheduled sweep kernels (warp per row,
-CTA band, band segment, cluster, level-synchronous pipeline); all of them keep
-the natural-order semantics of sym_gauss_seidel (amg.cpp:25-43).  Each is
-forced here (MPREC_GS_MODE) on a system large enough for the band kernels to
-engage, and the preconditioner apply / solve are checked against the oracle.
+The setup-time rule (amg_cycle.cu: tune_level_sweep) picks, per AMG level, one
+of the dependency-scheduled sweep kernels (level-synchronous programs with
+fixed-class, lane-group or variable-width records; thread-block cluster; warp
+per row); all of them keep the natural-order semantics of sym_gauss_seidel
+(amg.cpp:25-43).  Each is forced here (MPREC_GS_MODE, MPREC_GS_LS_REC,
+MPREC_LS_PAIRS) on config 2, and the preconditioner apply / solve are checked
+against the oracle.
 """
 import os
 
@@ -27,7 +28,7 @@ def cfg2():
     return gen.generate(2)
 
 
-@pytest.mark.parametrize("mode", ["warp", "cta", "seg", "cluster", "ls", "ls-fixed", "ls-var", "ls-push", ""])
+@pytest.mark.parametrize("mode", ["warp", "cluster", "ls", "ls-fixed", "ls-var", "ls-push", "ls-nopairs", ""])
 @pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
 def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
     if mode == "ls-push":
@@ -35,9 +36,10 @@ def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
         # switch is read once per process, so this case runs in its own interpreter
         pytest.skip("MPREC_LS_PUSH is read once per process: covered by test_ls_cluster_push_subprocess")
     if mode.startswith("ls-"):
-        # level-synchronous programs with fixed-class (k_gs_ls<ND>) or variable-width
-        # (k_gs_lsv) records on every level
-        monkeypatch.setenv("MPREC_GS_LS_REC", "1" if mode == "ls-fixed" else "2")
+        # level-synchronous programs with fixed-class (k_gs_ls<ND>), variable-width
+        # (k_gs_lsv) or -- auto without lane groups -- single-lane records
+        monkeypatch.setenv("MPREC_GS_LS_REC", {"ls-fixed": "1", "ls-var": "2"}.get(mode, "0"))
+        monkeypatch.setenv("MPREC_LS_PAIRS", "0" if mode == "ls-nopairs" else "1")
         mode = "ls"
     monkeypatch.setenv("MPREC_GS_MODE", mode)
     a, b, _ = cfg2
