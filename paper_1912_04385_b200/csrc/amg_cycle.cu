@@ -312,11 +312,12 @@ namespace mg {
 // groups, default 16, and MPREC_GS_LS_REC=0|1|2 auto / fixed-class / variable-
 // width records).
 static std::vector<int> ls_group_counts(int n) {
-    if (n >= (1 << 20)) return {74, 148, 37};
-    if (n >= 300000) return {148, 74, 37};
+    // c5 stage 0, r02 build (scripts/gs_ls_exp.py): 74 groups from level 0 down to
+    // 77k rows (level 3: 1.23 vs 1.32 ms at 148), 37 at ~35k, 4 below 20k rows
+    // (levels of 1.3k-15k rows: 0.026-0.132 ms vs 0.037-0.155 ms at 16-37)
     if (n >= 50000) return {74, 148, 37};
-    if (n >= 8192) return {37, 16, 8, 4};
-    return {16, 8, 4, 2, 1};  // small levels: one warp may beat any pipeline
+    if (n >= 20000) return {37, 16, 8, 4};
+    return {4, 8, 2, 1};
 }
 
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
