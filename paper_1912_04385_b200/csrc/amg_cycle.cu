@@ -303,21 +303,38 @@ namespace mg {
 // row's sum in different orders (the LS programs pre-scale by 1/a_ii and sum the
 // previous iterate's part first), so the choice is a fixed rule -- not timing --
 // and setups are bitwise reproducible:
-//   1. the level-synchronous programs (gs_ls.cu) with the first group count of
-//      ls_group_counts(n) that fits (B200 measurements);
+//   1. the level-synchronous programs (gs_ls.cu) with the first plan of
+//      ls_plans() that fits (B200 measurements);
 //   2. else the thread-block-cluster sweep (gs_cluster.cu) when the level's
 //      iterate fits one cluster's shared memory;
 //   3. else the warp-per-row sweep in topological claim order (k_gs).
 // MPREC_GS_MODE=warp | cluster | ls forces one (tests; `ls` with MPREC_GS_LS_K
-// groups, default 16, and MPREC_GS_LS_REC=0|1|2 auto / fixed-class / variable-
-// width records).
-static std::vector<int> ls_group_counts(int n) {
-    // c5 stage 0, r02 build (scripts/gs_ls_exp.py): 74 groups from level 0 down to
-    // 77k rows (level 3: 1.23 vs 1.32 ms at 148), 37 at ~35k, 4 below 20k rows
-    // (levels of 1.3k-15k rows: 0.026-0.132 ms vs 0.037-0.155 ms at 16-37)
-    if (n >= 50000) return {74, 148, 37};
-    if (n >= 20000) return {37, 16, 8, 4};
-    return {4, 8, 2, 1};
+// groups, default 16, MPREC_GS_LS_NW compute warps per group, default 1, and
+// MPREC_GS_LS_ND=0|2|4|8 dependency class, default 0 = from the level).
+struct LsPlan {
+    int K, nw;
+};
+// r = rows per DAG level.  Narrow levels run as ONE group (no boundary hops) on
+// 1-4 lockstep warps; wide levels as a pipeline of groups.  c5, r02 build
+// (scripts/gs_lw_exp.py; ms per forward sweep, previous kernel in brackets):
+//   r 1000 / 486 (levels 0, 1): 74 groups x 1 warp    0.48 / 0.55  [0.67 / 0.80]
+//   r 170 / 120  (levels 2, 3): 37 / 28 groups x 2    0.96 / 0.73  [1.58 / 1.22]
+//   r 87         (level 4):     1 group x 4 warps     0.47         [0.87]
+//   r 63         (level 5):     1 x 3                 0.23         [0.43]
+//   r 46 / 32    (levels 6, 7): 1 x 2                 0.11 / 0.07  [0.25 / 0.13]
+//   r <= 26      (levels 8+):   1 x 1                 0.04 ...     [0.06 ...]
+static std::vector<LsPlan> ls_plans(int n, int depth) {
+    const double r = double(n) / std::max(depth, 1);
+    std::vector<LsPlan> p;
+    if (r <= 26) p = {{1, 1}, {4, 1}};
+    else if (r <= 50) p = {{1, 2}, {4, 2}, {8, 1}};
+    else if (r <= 75) p = {{1, 3}, {4, 2}, {16, 2}};
+    else if (r <= 100) p = {{1, 4}, {24, 3}, {37, 2}};
+    else if (r <= 140) p = {{28, 2}, {37, 2}, {74, 1}};
+    else if (r <= 250) p = {{37, 2}, {56, 2}, {74, 1}};
+    else p = {{74, 1}, {148, 1}, {37, 2}};
+    for (LsPlan q : {LsPlan{74, 1}, LsPlan{37, 1}, LsPlan{16, 1}, LsPlan{8, 1}, LsPlan{4, 1}, LsPlan{1, 1}}) p.push_back(q);
+    return p;
 }
 
 void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
@@ -329,26 +346,30 @@ void tune_level_sweep(Ctx& c, AmgLevel& L, const Sched& sf, const Sched& sb) {
         return std::string(e ? e : "");
     }();
     if (force == "warp") return;
-    const bool have_lev = L.glev_f && L.glev_b;
+    auto env_int = [](const char* name, int dflt) {
+        const char* e = getenv(name);
+        return e ? atoi(e) : dflt;
+    };
     if (force == "ls") {
-        if (!have_lev || !csr_sorted(c, L.a)) return;
-        const int K = [] {
-            const char* e = getenv("MPREC_GS_LS_K");
-            return e ? atoi(e) : 16;
-        }();
-        const int rec = [] {
-            const char* e = getenv("MPREC_GS_LS_REC");
-            return e ? atoi(e) : 0;
-        }();
-        build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, rec, L.ls_fwd, L.ls_bwd);
+        if (!csr_sorted(c, L.a)) return;
+        build_ls_pair(c, L.a, L.invd.p, env_int("MPREC_GS_LS_K", 16), env_int("MPREC_GS_LS_NW", 1),
+                      env_int("MPREC_GS_LS_ND", 0), L.ls_fwd, L.ls_bwd);
         return;
     }
-    if (force.empty() && have_lev && L.n >= 512 && csr_sorted(c, L.a))
-        for (int K : ls_group_counts(L.n))
-            if (build_ls_pair(c, L.a, L.invd.p, L.glev_f, L.glev_b, K, 0, L.ls_fwd, L.ls_bwd)) {
-                if (trace_on()) fprintf(stderr, "[mprec] level n=%d sweep: level-sync K=%d\n", L.n, K);
+    if (force.empty() && L.n >= 512 && csr_sorted(c, L.a)) {
+        int lastK = -1, lastnw = -1;
+        for (LsPlan q : ls_plans(L.n, std::max(sf.nlev, sb.nlev))) {
+            if (q.K == lastK && q.nw == lastnw) continue;
+            lastK = q.K;
+            lastnw = q.nw;
+            if (L.n < 64 * q.K) continue;
+            if (build_ls_pair(c, L.a, L.invd.p, q.K, q.nw, 0, L.ls_fwd, L.ls_bwd)) {
+                if (trace_on())
+                    fprintf(stderr, "[mprec] level n=%d depth %d sweep: level-sync K=%d nw=%d\n", L.n, sf.nlev, q.K, q.nw);
                 return;
             }
+        }
+    }
     int cl_R = 0;
     const int cl_size = gs_cluster_plan(L.n, &cl_R);
     if (cl_size > 0 && (force.empty() || force == "cluster")) {

@@ -1,4 +1,4 @@
-// gs_ls.cu -- level-synchronous pipelined Gauss-Seidel sweep (K14, v2).
+// gs_ls.cu -- level-synchronous pipelined Gauss-Seidel sweep (K14).
 //
 // Same natural-order semantics as the other sweep kernels
 // (sym_gauss_seidel, amg.cpp:25-43): x_i = (b_i - sum_{k<i} a_ik x_k^new
@@ -6,33 +6,34 @@
 // backward.  What changes is how the dependency DAG is mapped onto the GPU:
 //
 //   * GROUPS.  The rows are cut into K contiguous ranges in sweep order, one
-//     thread block (one SM) each.  A group's rows are processed by ONE compute
-//     warp in global DAG-level order, <= 32 rows (one "step") at a time, with
-//     only a __syncwarp between steps: every dependency inside the group is a
-//     shared-memory read of a value the same warp wrote one or a few steps
-//     earlier.  The per-level cost is a few dependent instructions instead of
-//     a cross-SM hop (>= 0.38 us per hop).
+//     thread block (one SM) each.  A group's rows are processed by nw compute
+//     warps (usually one) in DAG-level order, <= 32 nw rows (one "step") at a
+//     time, with only a __syncwarp (nw > 1: a named barrier) between steps:
+//     every dependency inside the group is a shared-memory read of a value
+//     written one or a few steps earlier.  The per-level cost is a few dozen
+//     instructions instead of a cross-SM hop.
 //   * PIPELINE.  Dependencies may only cross into the previous group (checked
 //     at setup; the level falls back to the other kernels otherwise).  An
-//     importer warp polls the previous group's published values in the order
-//     they are produced and copies them into a shared-memory halo; the compute
-//     warp only checks a shared-memory counter.  The cross-SM latency is paid
-//     once per group boundary (pipeline fill), not once per DAG level.
+//     importer warp polls the previous group's published values and copies
+//     them into a shared-memory halo; the compute warps only check a
+//     shared-memory counter.  The cross-SM latency is paid once per group
+//     boundary (pipeline fill), not once per DAG level.  Narrow levels (few
+//     rows per DAG level) run as ONE group on one SM with no boundary at all.
 //   * PROGRAM.  Everything that does not depend on the sweep's new values --
 //     the row's coefficients pre-multiplied by 1/a_ii and the shared-memory
-//     slots of its dependencies -- is compiled at setup into a per-group
-//     stream of fixed-size chunks, in processing order, which a loader warp
+//     offsets of its dependencies -- is compiled at setup into a per-group
+//     stream of fixed-size steps, in processing order, which a loader warp
 //     streams into a shared-memory ring with 1-D TMA bulk copies
 //     (cp.async.bulk + mbarrier).  The part of each row that depends on the
 //     previous iterate, c'_i = (b_i - sum_old a_ik x_k^old) / a_ii, is computed
-//     by a fully parallel pre-pass straight into the chunks.
+//     by a fully parallel pre-pass straight into the program.
 //
-// Own-group values live in a ring of W slots indexed by processing position
-// (W > the largest position distance of a dependency + 32, checked at setup).
+// Own-group values live in a ring of W slots indexed by processing position.
 // Results differ from the warp-per-row sweep only by association (the old part
-// is summed first, coefficients are pre-scaled by 1/a_ii) and stay within the
-// 1e-10 apply bar.
+// is summed first, coefficients are pre-scaled by 1/a_ii, wide rows are summed
+// through partial nodes) and stay within the 1e-10 apply bar.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -44,9 +45,6 @@
 namespace mg {
 namespace {
 
-constexpr int kThreads = 96;  // warp 0: compute, warp 1: importer, warp 2: loader
-constexpr int kLsExportBit = 1 << 30;       // record myslot: row is read by the next group
-constexpr int kLsSlotMask = kLsExportBit - 1;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
@@ -99,133 +97,146 @@ __global__ void k_ls_pre(int n, const int* __restrict__ rp, const int* __restric
     if (o & 1) reinterpret_cast<unsigned long long*>(xnew)[i] = kPending;
 }
 
-// Step layout (16-byte aligned; a step never straddles a chunk):
-//   int4 {cnt, cls, need, bytes}     rows, dependency class, imports required, step size
-//   cnt lane records of RS(cls) bytes, record of lane q at 16 + q * RS:
-//     +0  int    sl[4]               shared-memory slots of dependencies 0..3
-//     +16 double c                   c'_i (written by the pre-pass)
-//     +24 int    row, myslot         output row, own ring slot
-//     +32 double e[ND]               a_ij / a_ii (0 for padding)
-//     +32+8ND int sl[4..ND)
-// The class is the step's widest row rounded up to ND = 2, 4, 8, 16, 32; the
-// record size has an odd number of 16-byte units so that the 32 lanes' 16-byte
-// loads are bank-conflict free.  A chunk starts with int4 {nsteps, 0, 0, 0}.
 __host__ __device__ constexpr int ls_nd(int cls) { return 2 << cls; }
-__host__ __device__ constexpr int ls_rs(int cls) {
-    return cls == 0 ? 48 : cls == 1 ? 80 : cls == 2 ? 112 : cls == 3 ? 208 : 400;
-}
 
-// dependency part of one row: x = c - sum_d e_d x_d (sequential for ND = 2,
-// a pairwise tree otherwise: depth log2(ND) + 2 instead of ND)
-template <int ND>
-__device__ __forceinline__ double ls_dot(const double* e, const double* xv, double c) {
-    if (ND == 2) return fma(-e[1], xv[1], fma(-e[0], xv[0], c));
-    double p[ND];
-#pragma unroll
-    for (int d = 0; d < ND; ++d) p[d] = e[d] * xv[d];
-#pragma unroll
-    for (int w = ND / 2; w >= 1; w /= 2)
-#pragma unroll
-        for (int d = 0; d < w; ++d) p[d] += p[d + w];
-    return c - p[0];
-}
+// ---------------------------------------------------------------------------
+// Fixed-format warp-steps (k_gs_lw).  Same groups, pipeline and pre-pass as
+// above; what changes is the program format and the step loop.  A lone warp
+// pays ~5-10 cycles per issued instruction, so k_gs_ls's ~120 SASS instructions
+// per step cost 0.2-0.4 us per DAG level; here a step is ~25-45 instructions:
+//   * a step is nw WARP BLOCKS of fixed size (one per compute warp), each an
+//     array of 16-byte vectors over the 32 lanes (every load a conflict-free
+//     lane-strided LDS.128): ND/2 vectors of coefficients a_ij / a_ii, one tail
+//     vector {c', row, packed}, ND 32-bit byte offsets of the dependencies in
+//     the value area.  No headers, no variable sizes, a fixed number of steps
+//     per chunk (the inner loop is fully unrolled, every program address an
+//     immediate); the record of step s + 1 is loaded into registers while step
+//     s waits for its dependency values, which are the only loads left on the
+//     step-to-step chain.
+//   * packed = own byte offset in the value area (17 bits) | imports needed (15).
+//   * NODES instead of lane groups: a row with more than ND dependencies becomes
+//     a two-level tree -- partial nodes summing its earliest-available
+//     dependencies (scheduled in earlier steps, in otherwise idle lanes, value
+//     kept in the ring only) and a final node of <= ND inputs.  The node DAG is
+//     re-levelled on the host; no shuffles in the step loop.
+//   * the compute warps never touch an mbarrier: a publisher warp waits for the
+//     bulk copies and advances a `loaded` chunk counter (checked once per
+//     chunk), the compute warps publish `consumed` chunk counters the loader
+//     polls before it refills a ring slot.
+//   * nw > 1 (MULTI): the compute warps run in lockstep, one named barrier per
+//     step (measured slower per step: the warps share the SM's one shared-memory
+//     pipe; kept for levels whose groups would otherwise need several steps per
+//     DAG level).
+// Padding lanes and padding steps: zero coefficients, the zero slot, row -1,
+// the trash slot.
+__host__ __device__ constexpr int lw_wb(int nd) { return nd == 2 ? 1280 : nd == 4 ? 2048 : 3584; }
+__host__ __device__ constexpr int lw_tail(int nd) { return (nd / 2) * 512; }
+__host__ __device__ constexpr int lw_off(int nd) { return (nd / 2) * 512 + 512; }
+__host__ __device__ constexpr int lw_spc(int nd) { return nd == 8 ? 4 : 8; }  // steps per chunk
+constexpr int kLwOwnBits = 17;
 
 template <int ND>
-__device__ __forceinline__ void ls_slots(const char* rec, int* sl) {
-    const int4 q = *reinterpret_cast<const int4*>(rec);
-    sl[0] = q.x;
-    sl[1] = q.y;
-    if (ND > 2) {
-        sl[2] = q.z;
-        sl[3] = q.w;
+struct LwRec {
+    double e[ND];
+    unsigned off[ND];
+    double c;
+    int row;
+    unsigned packed;
+};
+
+template <int ND>
+__device__ __forceinline__ void lw_load(unsigned wb, int lane, LwRec<ND>& r) {  // wb: the warp block
+    const unsigned a = wb + 16u * unsigned(lane);
+#pragma unroll
+    for (int v = 0; v < ND / 2; ++v)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.e[2 * v]), "=d"(r.e[2 * v + 1]) : "r"(a + 512 * v));
+    unsigned lo, hi;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(lo), "=r"(hi), "=r"(r.row), "=r"(r.packed)
+                 : "r"(a + lw_tail(ND)));
+    r.c = __hiloint2double(int(hi), int(lo));
+    if (ND == 2) {
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                     : "=r"(r.off[0]), "=r"(r.off[1])
+                     : "r"(wb + lw_off(ND) + 8u * unsigned(lane)));
+    } else {
+#pragma unroll
+        for (int v = 0; v < ND / 4; ++v)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(r.off[4 * v]), "=r"(r.off[4 * v + 1]), "=r"(r.off[4 * v + 2]), "=r"(r.off[4 * v + 3])
+                         : "r"(a + lw_off(ND) + 512 * v));
     }
-#pragma unroll
-    for (int d = 4; d < ND; d += 4) {
-        const int4 r = reinterpret_cast<const int4*>(rec + 32 + 8 * ND)[(d - 4) / 4];
-        sl[d] = r.x;
-        sl[d + 1] = r.y;
-        sl[d + 2] = r.z;
-        sl[d + 3] = r.w;
-    }
 }
 
-// One thread block per group; ND (the level's widest row, rounded up) is a
-// template parameter so the step loop has no class switch.
-template <int ND>
-__global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ prog, const int2* __restrict__ gch,
-                                                        const int* __restrict__ imp, const int2* __restrict__ gimp,
-                                                        double* xnew, int W, int trash, int ns, long long* stats,
-                                                        int push) {
-    constexpr int RS = ls_rs(ND == 2 ? 0 : ND == 4 ? 1 : ND == 8 ? 2 : ND == 16 ? 3 : 4);
+// wait until the shared-memory counter at `a` reaches `want` (warp-uniform)
+__device__ __forceinline__ void lw_wait(unsigned a, int want, int& have) {
+    asm volatile(
+        "{\n .reg .pred p;\n .reg .s32 r;\n"
+        " setp.le.s32 p, %2, %0;\n"
+        " @p bra.uni LWD%=;\n"
+        "LWW%=:\n ld.volatile.shared.s32 r, [%1];\n setp.lt.s32 p, r, %2;\n @p bra.uni LWW%=;\n"
+        " mov.s32 %0, r;\n fence.acq_rel.cta;\n"
+        "LWD%=:\n}"
+        : "+r"(have)
+        : "r"(a), "r"(want)
+        : "memory");
+}
+
+template <int ND, bool MULTI>
+__global__ void __launch_bounds__(352, 1) k_gs_lw(const char* __restrict__ prog, const int2* __restrict__ gch,
+                                                   const int* __restrict__ imp, const int2* __restrict__ gimp,
+                                                   double* xnew, int W, int hmax, int ns, int nw, long long* stats) {
+    constexpr int WB = lw_wb(ND), SPC = lw_spc(ND);
     extern __shared__ __align__(128) unsigned char sm[];
+    const int stepb = MULTI ? nw * WB : WB, chb = SPC * stepb;
     char* ring = reinterpret_cast<char*>(sm);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ns * kLsCH);
-    uint64_t* empty = full + ns;
-    int* imported = reinterpret_cast<int*>(empty + ns);
-    double* xs = reinterpret_cast<double*>(sm + ns * kLsCH + 2 * ns * 8 + 16);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ns * chb);
+    int* ctr = reinterpret_cast<int*>(full + ns);  // [0] imported, [1] chunks loaded, [2 + w] chunks consumed by warp w
+    double* xs = reinterpret_cast<double*>(sm + ns * chb + ns * 8 + 64);
     const int g = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int2 ch = gch[g];  // first chunk, chunk count
+    const int2 ch = gch[g];  // first chunk, chunks
+    const int nch = ch.y;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < ns; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
-        }
-        *imported = 0;
+        for (int s = 0; s < ns; ++s) mbar_init(full + s, 1);
+        for (int q = 0; q < 16; ++q) ctr[q] = 0;
         xs[W] = 0.0;  // zero slot (padding dependencies)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // cluster push (launched as clusters of 2): the even CTA of a pair stores its
-    // exported values straight into the odd CTA's halo (DSMEM), whose importer
-    // then only polls shared memory; the halo starts as kPending in every thread
-    // block and a cluster barrier orders that before any remote store
-    const bool pushed_in = push && (g & 1);  // my halo is written by my cluster peer
-    if (pushed_in) {
-        const int nimp = gimp[g].y;
-        for (int i = threadIdx.x; i < nimp; i += blockDim.x)
-            reinterpret_cast<unsigned long long*>(xs + W + 1)[i] = kPending;
-    }
     __syncthreads();
-    if (push) {
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    }
-    if (warp == 2) {  // loader: program chunks -> shared-memory ring (1-D TMA bulk copies)
-        if (lane == 0)
-            for (int c = 0; c < ch.y; ++c) {
-                const int s = c & (ns - 1);
-                if (c >= ns) mbar_wait(empty + s, ((c / ns) - 1) & 1);
-                mbar_expect_tx(full + s, kLsCH);
-                bulk_g2s(ring + s * kLsCH, prog + (int64_t)(ch.x + c) * kLsCH, kLsCH, full + s);
-            }
-        return;
-    }
-    if (warp == 1 && pushed_in) {  // importer, cluster push: poll the local halo
-        const int nimp = gimp[g].y;
-        volatile unsigned long long* halo = reinterpret_cast<volatile unsigned long long*>(xs + W + 1);
-        volatile int* vimp = imported;
-        int base = 0;
-        while (base < nimp) {
-            const int idx = base + lane;
-            const bool ready = idx < nimp && halo[idx] != kPending;
-            const unsigned m = __ballot_sync(0xffffffffu, ready);
-            const int pre = min(m == 0xffffffffu ? 32 : __ffs(~m) - 1, nimp - base);
-            if (pre > 0) {
-                if (lane == 0) {
-                    asm volatile("fence.acq_rel.cluster;" ::: "memory");
-                    *vimp = base + pre;
+    if (warp == nw + 1) {  // loader: program chunks -> ring, refilling a slot once every compute warp released it
+        if (lane == 0) {
+            volatile int* cons = ctr + 2;
+            for (int c = 0; c < nch; ++c) {
+                const int s = c % ns;
+                if (c >= ns) {
+                    for (int w = 0; w < nw; ++w)
+                        while (cons[w] < c - ns + 1) __nanosleep(32);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
-                base += pre;
+                mbar_expect_tx(full + s, chb);
+                bulk_g2s(ring + s * chb, prog + (int64_t)(ch.x + c) * chb, chb, full + s);
             }
         }
         return;
     }
-    if (warp == 1) {  // importer: previous group's values -> halo, in production order
+    if (warp == nw + 2) {  // publisher: completed bulk copies -> `loaded` chunk counter
+        if (lane == 0) {
+            volatile int* ld = ctr + 1;
+            for (int c = 0; c < nch; ++c) {
+                mbar_wait(full + (c % ns), (c / ns) & 1);
+                __threadfence_block();
+                *ld = c + 1;
+            }
+        }
+        return;
+    }
+    if (warp == nw) {  // importer: previous group's values -> halo, in production order
         const int2 gi = gimp[g];
         const int* rows = imp + gi.x;
         const int nimp = gi.y;
         volatile double* halo = xs + W + 1;
-        volatile int* vimp = imported;
+        volatile int* vimp = ctr;
         int base = 0;
         while (base < nimp) {
             const int idx = base + lane;
@@ -247,299 +258,75 @@ __global__ void __launch_bounds__(kThreads, 1) k_gs_ls(const char* __restrict__ 
         }
         return;
     }
-    // compute warp.  Software pipeline: at step k the registers of step k
-    // (header, slots) are already loaded; the next header and slots are issued
-    // right after this step's dependency loads, so the only latencies left on the
-    // critical path are LDS(dependencies) -> FMAs -> STS.  The import wait is a
-    // warp-uniform loop inside one asm block, padding lanes read a valid record
-    // (min(lane, cnt - 1)) and their stores are predicated off: no divergent branch.
-    const volatile double* vxs = xs;
-    const unsigned imp_a = smem_u32(imported);
-    int have = 0;
-    long long t_start = 0;
+    // compute warps
+    const unsigned xs_a = smem_u32(xs);
+    const unsigned imp_a = smem_u32(ctr), ld_a = imp_a + 4, cons_a = imp_a + 8 + 4 * warp;
+    const unsigned ring_a = smem_u32(ring) + unsigned(warp) * WB;
+    double* xg = xnew;
+    asm volatile("" : "+l"(xg));  // keep the pointer in registers (no constant-bank reload per step)
+    int have_imp = 0, have_ld = 0, slot = 0;
+    long long t_start = 0, t_first = 0;
     if (stats) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    // cluster push target: the peer CTA's halo (shared::cluster address)
-    const bool push_out = push && !(g & 1) && g + 1 < int(gridDim.x);
-    unsigned peer_halo = 0;
-    int nexp = 0;
-    if (push_out)
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer_halo) : "r"(smem_u32(xs + W + 1)), "r"(1));
-    for (int c = 0; c < ch.y; ++c) {
-        const int slot = c & (ns - 1);
-        mbar_wait(full + slot, (c / ns) & 1);
-        const char* st = ring + slot * kLsCH;
-        const int nsteps = *reinterpret_cast<const int*>(st);
-        st += 16;
-        int4 h = *reinterpret_cast<const int4*>(st);
-        int sl[ND];
-        ls_slots<ND>(st + 16 + min(lane, h.x - 1) * RS, sl);
-        for (int k = 0; k < nsteps; ++k) {
-            asm volatile(
-                "{\n .reg .pred p;\n .reg .s32 r;\n"
-                " setp.le.s32 p, %2, %0;\n"
-                " @p bra.uni LSD%=;\n"
-                "LSW%=:\n ld.volatile.shared.s32 r, [%1];\n setp.lt.s32 p, r, %2;\n @p bra.uni LSW%=;\n"
-                " mov.s32 %0, r;\n fence.acq_rel.cta;\n"
-                "LSD%=:\n}"
-                : "+r"(have)
-                : "r"(imp_a), "r"(h.z)
-                : "memory");
-            const char* rec = st + 16 + min(lane, h.x - 1) * RS;
-            // next step's header first: its slots can then be loaded while this
-            // step's dependencies are summed (garbage after the chunk's last step)
-            const char* stn = st + h.w;
-            int4 hn;
-            asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(hn.x), "=r"(hn.y), "=r"(hn.z), "=r"(hn.w)
-                         : "r"(smem_u32(stn)));
+    LwRec<ND> R;
+    for (int c = 0; c < nch; ++c) {
+        // this chunk and the next one (its first record is prefetched at this chunk's last step)
+        lw_wait(ld_a, min(nch, c + 2), have_ld);
+        const unsigned base = ring_a + unsigned(slot) * unsigned(chb);
+        slot = slot + 1 == ns ? 0 : slot + 1;
+        const unsigned nbase = c + 1 < nch ? ring_a + unsigned(slot) * unsigned(chb) : base;
+        if (c == 0) lw_load<ND>(base, lane, R);
+#pragma unroll
+        for (int k = 0; k < SPC; ++k) {
+            lw_wait(imp_a, int(R.packed >> kLwOwnBits), have_imp);
+            if (MULTI)
+                asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+            else
+                __syncwarp();
             double xv[ND];
 #pragma unroll
-            for (int d = 0; d < ND; ++d) MG_DCHECK(sl[d] >= 0 && sl[d] < trash);
-            MG_DCHECK(h.x >= 1 && h.x <= 32 && h.w >= 16 && h.w <= kLsCH && h.z >= 0 && h.z <= trash - W - 1);
-#pragma unroll
-            for (int d = 0; d < ND; ++d) xv[d] = vxs[sl[d]];
-            const bool more = k + 1 < nsteps;  // (select, not a branch)
-            ls_slots<ND>((more ? stn : st) + 16 + min(lane, (more ? hn.x : h.x) - 1) * RS, sl);
-            const double cc = *reinterpret_cast<const double*>(rec + 16);
-            const int2 rs = *reinterpret_cast<const int2*>(rec + 24);
-            double e[ND];
-#pragma unroll
-            for (int d = 0; d < ND; d += 2) {
-                const double2 q = reinterpret_cast<const double2*>(rec + 32)[d / 2];
-                e[d] = q.x;
-                e[d + 1] = q.y;
+            for (int d = 0; d < ND; ++d) {
+                MG_DCHECK(R.off[d] <= 8u * unsigned(W + 1 + hmax) && (R.off[d] & 7u) == 0);
+                asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(xv[d]) : "r"(xs_a + R.off[d]) : "memory");
             }
-            double x = ls_dot<ND>(e, xv, cc);
-            // lane groups (header .y: pairs << 8 | quads << 16): quads on lanes
-            // [0, 4 nq), pairs on [4 nq, 4 nq + 2 np); the group's other lanes hold
-            // -(sums of further dependencies) with c' = 0
-            if (h.y >> 8) {
-                const int nq = (h.y >> 16) & 0xff, np2 = 4 * nq + 2 * ((h.y >> 8) & 0xff);
-                const double o1 = __shfl_xor_sync(0xffffffffu, x, 1);
-                if (lane < np2) x += o1;
-                if (nq) {
-                    const double o2 = __shfl_xor_sync(0xffffffffu, x, 2);
-                    if (lane < 4 * nq) x += o2;
-                }
+            LwRec<ND> N;
+            lw_load<ND>(k + 1 < SPC ? base + unsigned(k + 1) * unsigned(stepb) : nbase, lane, N);
+            // x = c' - sum_d e_d x_d as a tree of depth <= 4
+            double x;
+            if (ND == 2) {
+                x = fma(-R.e[1], xv[1], fma(-R.e[0], xv[0], R.c));
+            } else if (ND == 4) {
+                const double t0 = fma(-R.e[1], xv[1], fma(-R.e[0], xv[0], R.c));
+                const double t1 = fma(R.e[3], xv[3], R.e[2] * xv[2]);
+                x = t0 - t1;
+            } else {
+                const double t0 = fma(-R.e[1], xv[1], fma(-R.e[0], xv[0], R.c));
+                const double t1 = fma(R.e[3], xv[3], R.e[2] * xv[2]);
+                const double t2 = fma(R.e[5], xv[5], R.e[4] * xv[4]);
+                const double t3 = fma(R.e[7], xv[7], R.e[6] * xv[6]);
+                x = (t0 - t1) - (t2 + t3);
             }
-            const int row = lane < h.x ? rs.x : -1;
-            MG_DCHECK(lane >= h.x || rs.x < 0 || (rs.y & kLsSlotMask) < W);
-            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(
-                             smem_u32(xs + (lane < h.x ? (rs.y & kLsSlotMask) : trash))),
-                         "d"(x)
-                         : "memory");
+            const unsigned own = R.packed & ((1u << kLwOwnBits) - 1);
+            MG_DCHECK(own <= 8u * unsigned(W + 1 + hmax) && (R.row < 0 || own < 8u * unsigned(W)));
+            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(xs_a + own), "d"(x) : "memory");
             asm volatile(
-                "{\n .reg .pred p;\n setp.ge.s32 p, %2, 0;\n @p st.relaxed.gpu.global.b64 [%0], %1;\n}" ::"l"(xnew + row),
-                "l"(__double_as_longlong(x)), "r"(row)
+                "{\n .reg .pred p;\n setp.ge.s32 p, %2, 0;\n @p st.relaxed.gpu.global.b64 [%0], %1;\n}" ::"l"(xg + R.row),
+                "l"(__double_as_longlong(x)), "r"(R.row)
                 : "memory");
-            if (push_out) {
-                // exported rows arrive in the peer's import order (processing order)
-                const bool ex = lane < h.x && (rs.y & kLsExportBit);
-                const unsigned m = __ballot_sync(0xffffffffu, ex);
-                const int hidx = nexp + __popc(m & ((1u << lane) - 1));
-                asm volatile(
-                    "{\n .reg .pred p;\n setp.ne.s32 p, %2, 0;\n"
-                    " @p st.relaxed.cluster.shared::cluster.b64 [%0], %1;\n}" ::"r"(peer_halo + 8u * unsigned(hidx)),
-                    "l"(__double_as_longlong(x)), "r"(int(ex))
-                    : "memory");
-                nexp += __popc(m);
-            }
-            __syncwarp();
-            st = stn;
-            h = hn;
+            R = N;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + slot);
+        if (lane == 0) asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(cons_a), "r"(c + 1) : "memory");
+        if (stats && c == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_first));
     }
-    if (stats && lane == 0) {
+    if (stats && threadIdx.x == 0) {  // diagnostics: group start, end of its first chunk, end
         long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         stats[4 * g + 0] = t_start;
         stats[4 * g + 1] = t_end;
-        stats[4 * g + 2] = 0;
-        stats[4 * g + 3] = 0;
+        stats[4 * g + 2] = t_first - t_start;
+        stats[4 * g + 3] = nch * SPC;
     }
 }
 
-// Variable-width records (levels whose widest row has more than 4
-// dependencies): the step header's class field is nd4 = ceil(widest row / 4),
-// the record of lane q is
-//   +0 int4 sl[0..3] | +16 double c' | +24 int row, myslot | +32 double e[0..3]
-//   +64 + 48 (g - 1): int4 sl[4g..4g+3], double e[4g..4g+3]    (g = 1 .. nd4 - 1)
-// padded to an odd number of 16-byte units (conflict-free lane-strided loads).
-// Only the step's own width is loaded and summed (warp-uniform group loop), so
-// a few wide rows no longer widen every record of the level.
-__host__ __device__ constexpr int ls_rsv(int nd4) {
-    return (16 + 48 * nd4) + ((((16 + 48 * nd4) >> 4) & 1) ? 0 : 16);
-}
-
-__device__ __forceinline__ double ls_quad(const volatile double* xs, int4 sl, const double* e) {
-    const double x0 = xs[sl.x], x1 = xs[sl.y], x2 = xs[sl.z], x3 = xs[sl.w];
-    const double2 a = reinterpret_cast<const double2*>(e)[0], b = reinterpret_cast<const double2*>(e)[1];
-    return fma(a.x, x0, a.y * x1) + fma(b.x, x2, b.y * x3);
-}
-
-// dependency groups 1 .. NQ-1 of a variable-width record (NQ = the step's nd4)
-template <int NQ>
-__device__ __forceinline__ double lsv_rest(const char* rec, const volatile double* xs) {
-    constexpr int M = NQ - 1;
-    int4 sq[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) sq[q] = *reinterpret_cast<const int4*>(rec + 64 + 48 * q);
-    double xv[4 * M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
-        xv[4 * q] = xs[sq[q].x];
-        xv[4 * q + 1] = xs[sq[q].y];
-        xv[4 * q + 2] = xs[sq[q].z];
-        xv[4 * q + 3] = xs[sq[q].w];
-    }
-    double p[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
-        const double2 a = reinterpret_cast<const double2*>(rec + 64 + 48 * q + 16)[0];
-        const double2 b = reinterpret_cast<const double2*>(rec + 64 + 48 * q + 16)[1];
-        p[q] = fma(a.x, xv[4 * q], a.y * xv[4 * q + 1]) + fma(b.x, xv[4 * q + 2], b.y * xv[4 * q + 3]);
-    }
-#pragma unroll
-    for (int w = 1; w < M; w *= 2)
-#pragma unroll
-        for (int q = 0; q + w < M; q += 2 * w) p[q] += p[q + w];
-    return p[0];
-}
-
-__global__ void __launch_bounds__(kThreads, 1) k_gs_lsv(const char* __restrict__ prog, const int2* __restrict__ gch,
-                                                         const int* __restrict__ imp, const int2* __restrict__ gimp,
-                                                         double* xnew, int W, int trash, int ns) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    char* ring = reinterpret_cast<char*>(sm);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + ns * kLsCH);
-    uint64_t* empty = full + ns;
-    int* imported = reinterpret_cast<int*>(empty + ns);
-    double* xs = reinterpret_cast<double*>(sm + ns * kLsCH + 2 * ns * 8 + 16);
-    const int g = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int2 ch = gch[g];
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < ns; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
-        }
-        *imported = 0;
-        xs[W] = 0.0;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == 2) {
-        if (lane == 0)
-            for (int c = 0; c < ch.y; ++c) {
-                const int s = c & (ns - 1);
-                if (c >= ns) mbar_wait(empty + s, ((c / ns) - 1) & 1);
-                mbar_expect_tx(full + s, kLsCH);
-                bulk_g2s(ring + s * kLsCH, prog + (int64_t)(ch.x + c) * kLsCH, kLsCH, full + s);
-            }
-        return;
-    }
-    if (warp == 1) {
-        const int2 gi = gimp[g];
-        const int* rows = imp + gi.x;
-        const int nimp = gi.y;
-        volatile double* halo = xs + W + 1;
-        volatile int* vimp = imported;
-        int base = 0;
-        while (base < nimp) {
-            const int idx = base + lane;
-            const bool in = idx < nimp;
-            unsigned long long raw = kPending;
-            if (in) raw = ld_relaxed_ls(xnew + __ldg(rows + idx));
-            const bool ready = in && raw != kPending;
-            const unsigned m = __ballot_sync(0xffffffffu, ready);
-            const int pre = min(m == 0xffffffffu ? 32 : __ffs(~m) - 1, nimp - base);
-            if (lane < pre) halo[idx] = __longlong_as_double((long long)raw);
-            if (pre > 0) {
-                __syncwarp();
-                if (lane == 0) {
-                    __threadfence_block();
-                    *vimp = base + pre;
-                }
-                base += pre;
-            }
-        }
-        return;
-    }
-    const volatile double* vxs = xs;
-    const unsigned imp_a = smem_u32(imported);
-    int have = 0;
-    for (int c = 0; c < ch.y; ++c) {
-        const int slot = c & (ns - 1);
-        mbar_wait(full + slot, (c / ns) & 1);
-        const char* st = ring + slot * kLsCH;
-        const int nsteps = *reinterpret_cast<const int*>(st);
-        st += 16;
-        int4 h = *reinterpret_cast<const int4*>(st);
-        int4 s0 = *reinterpret_cast<const int4*>(st + 16 + min(lane, h.x - 1) * ls_rsv(h.y));
-        for (int k = 0; k < nsteps; ++k) {
-            asm volatile(
-                "{\n .reg .pred p;\n .reg .s32 r;\n"
-                " setp.le.s32 p, %2, %0;\n"
-                " @p bra.uni LSD%=;\n"
-                "LSW%=:\n ld.volatile.shared.s32 r, [%1];\n setp.lt.s32 p, r, %2;\n @p bra.uni LSW%=;\n"
-                " mov.s32 %0, r;\n fence.acq_rel.cta;\n"
-                "LSD%=:\n}"
-                : "+r"(have)
-                : "r"(imp_a), "r"(h.z)
-                : "memory");
-            const char* rec = st + 16 + min(lane, h.x - 1) * ls_rsv(h.y);
-            // next step: header first, then (below) its first slot group
-            const char* stn = st + h.w;
-            int4 hn;
-            asm volatile("ld.volatile.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(hn.x), "=r"(hn.y), "=r"(hn.z), "=r"(hn.w)
-                         : "r"(smem_u32(stn)));
-            MG_DCHECK(s0.x >= 0 && s0.x < trash && s0.y >= 0 && s0.y < trash && s0.z >= 0 && s0.z < trash &&
-                      s0.w >= 0 && s0.w < trash);
-            MG_DCHECK(h.x >= 1 && h.x <= 32 && h.y >= 1 && h.y <= 8 && h.w >= 16 && h.w <= kLsCH);
-            const double x0 = vxs[s0.x], x1 = vxs[s0.y], x2 = vxs[s0.z], x3 = vxs[s0.w];
-            const bool more = k + 1 < nsteps;
-            const int4 s0n = *reinterpret_cast<const int4*>((more ? stn : st) + 16 +
-                                                           min(lane, (more ? hn.x : h.x) - 1) *
-                                                               ls_rsv(more ? hn.y : h.y));
-            const double cc = *reinterpret_cast<const double*>(rec + 16);
-            const int2 rs = *reinterpret_cast<const int2*>(rec + 24);
-            const double2 ea = reinterpret_cast<const double2*>(rec + 32)[0], eb = reinterpret_cast<const double2*>(rec + 32)[1];
-            // groups 1 .. nd4-1: one warp-uniform switch on the step's width, then
-            // straight-line loads (all slots, all values) and a pairwise tree
-            double rest;
-            switch (h.y) {
-                case 1: rest = 0.0; break;
-                case 2: rest = lsv_rest<2>(rec, vxs); break;
-                case 3: rest = lsv_rest<3>(rec, vxs); break;
-                case 4: rest = lsv_rest<4>(rec, vxs); break;
-                case 5: rest = lsv_rest<5>(rec, vxs); break;
-                case 6: rest = lsv_rest<6>(rec, vxs); break;
-                case 7: rest = lsv_rest<7>(rec, vxs); break;
-                default: rest = lsv_rest<8>(rec, vxs); break;
-            }
-            const double acc = (fma(ea.x, x0, ea.y * x1) + fma(eb.x, x2, eb.y * x3)) + rest;
-            const double x = cc - acc;
-            const int row = lane < h.x ? rs.x : -1;
-            asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(
-                             smem_u32(xs + (lane < h.x ? (rs.y & kLsSlotMask) : trash))),
-                         "d"(x)
-                         : "memory");
-            asm volatile(
-                "{\n .reg .pred p;\n setp.ge.s32 p, %2, 0;\n @p st.relaxed.gpu.global.b64 [%0], %1;\n}" ::"l"(xnew + row),
-                "l"(__double_as_longlong(x)), "r"(row)
-                : "memory");
-            __syncwarp();
-            st = stn;
-            h = hn;
-            s0 = s0n;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + slot);
-    }
-}
 
 __global__ void k_ls_testvec(double* b, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -549,24 +336,20 @@ __global__ void k_ls_testvec(double* b, int n) {
 
 }  // namespace
 
-int ls_smem_bytes(int W, int hmax, int ns) { return ns * kLsCH + 2 * ns * 8 + 16 + (W + 2 + hmax) * 8; }
-
-// Build the group programs of one sweep direction.  Returns false (and leaves
-// s.ok = false) when the level does not fit the scheme: a dependency reaching
-// beyond the previous group, or a ring + halo larger than shared memory.
-// Host-side program of one sweep direction (built from a host copy of the level).
 struct LsBuilt {
     bool ok = false;
     int K = 0, W = 0, hmax = 0, dir = 0, nsteps = 0, nchunks = 0, maxdist = 0, nd = 0, ns = 0, cls = 0;
+    int nw = 0, spc = 0, chb = 0;  // fixed-format warp-steps (k_gs_lw)
     std::vector<char> prog;
     std::vector<int2> gch, gimp;
     std::vector<int> imp;
     std::vector<long long> coff;
 };
 
-static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci, const std::vector<double>& v,
-                          const std::vector<int>& lev, const std::vector<double>& invd, int n, int dir, int K,
-                          int rec_mode, LsBuilt& out) {
+// Fixed-format warp-step programs (k_gs_lw) of one sweep direction.  nw compute
+// warps per group; ndsel 0: dependency class chosen from the level, 1/2/3: ND = 2/4/8.
+static void ls_build_lw(const std::vector<int>& rp, const std::vector<int>& ci, const std::vector<double>& v,
+                        const std::vector<double>& invd, int n, int dir, int K, int nw, int ndsel, LsBuilt& out) {
     out = LsBuilt();
     if (n < 64 || K < 1) return;
     K = std::min(K, n / 32);
@@ -577,212 +360,289 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
     for (int g = 0; g <= K; ++g) gstart[g] = int((int64_t)g * n / K);
     for (int g = 0; g < K; ++g)
         for (int t = gstart[g]; t < gstart[g + 1]; ++t) gid[row_of_t(t)] = g;
-    for (int i = 0; i < n; ++i)
+    std::vector<int> nd(n, 0);
+    int maxnd = 0;
+    int64_t sumnd = 0;
+    for (int i = 0; i < n; ++i) {
         for (int k = rp[i]; k < rp[i + 1]; ++k) {
             const int j = ci[k];
-            if (is_dep(i, j) && gid[j] != gid[i] && gid[j] != gid[i] - 1) return;
+            if (!is_dep(i, j)) continue;
+            if (gid[j] != gid[i] && gid[j] != gid[i] - 1) return;  // beyond the previous group
+            ++nd[i];
         }
-    auto ndeps = [&](int i) {
-        int d = 0;
-        for (int k = rp[i]; k < rp[i + 1]; ++k) d += is_dep(i, ci[k]) ? 1 : 0;
-        return d;
-    };
-    std::vector<int> nd(n);
-    int maxnd = 0;
-    for (int i = 0; i < n; ++i) maxnd = std::max(maxnd, nd[i] = ndeps(i));
-    if (maxnd > 32) return;
-    // processing order inside each group: (level, dependency count, sweep index) --
-    // sorting a level's rows by width keeps wide rows together in few steps
-    std::vector<int> seq(n), pos(n);
-    for (int g = 0; g < K; ++g) {
-        int* q = seq.data() + gstart[g];
-        const int m = gstart[g + 1] - gstart[g];
-        for (int u = 0; u < m; ++u) q[u] = row_of_t(gstart[g] + u);
-        std::stable_sort(q, q + m, [&](int x, int y) { return lev[x] != lev[y] ? lev[x] < lev[y] : nd[x] < nd[y]; });
-        for (int u = 0; u < m; ++u) pos[q[u]] = u;
+        maxnd = std::max(maxnd, nd[i]);
+        sumnd += nd[i];
     }
-    // import lists (previous group's rows, in its processing order) and halo indices
-    std::vector<int> hidx(n, -1), gimp_off(K + 1, 0), imp;
+    // dependency class: ND >= the widest row when that is <= 4; else 8 (wider rows
+    // become trees of partial nodes).  A two-level tree holds ND * ND dependencies.
+    int ND = ndsel == 1 ? 2 : ndsel == 2 ? 4 : ndsel == 3 ? 8 : maxnd <= 2 ? 2 : maxnd <= 4 ? 4 : 8;
+    if (maxnd > ND * ND) ND = 8;
+    if (maxnd > ND * ND) return;
+    const int cls = ND == 2 ? 0 : ND == 4 ? 1 : 2;
+    // ---- nodes: id < n is row id's final node, id >= n a partial node.  Expanded
+    // rows keep their inputs in (xsrc, xcoef): src >= 0 a row's value, src < 0 the
+    // partial node n + (-1 - src)
+    struct Part {
+        int owner, lev, first, cnt;
+    };
+    std::vector<Part> parts;
+    std::vector<int> xfirst(n, -1), xcnt(n, 0), xsrc;
+    std::vector<double> xcoef;
+    std::vector<int> rlev(n, 0);
+    {
+        std::vector<std::pair<int, int>> dl;  // (level of the dependency, k)
+        for (int t = 0; t < n; ++t) {
+            const int i = row_of_t(t);
+            int lv = 0;
+            if (nd[i] <= ND) {
+                for (int k = rp[i]; k < rp[i + 1]; ++k)
+                    if (is_dep(i, ci[k])) lv = std::max(lv, rlev[ci[k]] + 1);
+                rlev[i] = lv;
+                continue;
+            }
+            dl.clear();
+            for (int k = rp[i]; k < rp[i + 1]; ++k)
+                if (is_dep(i, ci[k])) dl.emplace_back(rlev[ci[k]], k);
+            std::stable_sort(dl.begin(), dl.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+            const int m = int(dl.size());
+            const int P = (m - ND + (ND - 2)) / (ND - 1);  // partial nodes
+            const int direct = ND - P;                     // latest dependencies stay direct
+            const int npd = m - direct;                    // dependencies summed by partial nodes
+            xfirst[i] = int(xsrc.size());
+            int at = 0;
+            // layout in xsrc for row i: [final node inputs: P partial refs + direct deps][partial 0 deps][partial 1 deps]...
+            const int pbase = int(parts.size());
+            for (int p = 0; p < P; ++p) {
+                xsrc.push_back(-1 - (pbase + p));
+                xcoef.push_back(1.0);
+            }
+            for (int q = npd; q < m; ++q) {
+                xsrc.push_back(ci[dl[q].second]);
+                xcoef.push_back(v[dl[q].second] * invd[i]);
+                lv = std::max(lv, dl[q].first + 1);
+            }
+            xcnt[i] = P + direct;
+            at = 0;
+            for (int p = 0; p < P; ++p) {
+                const int cnt = std::min(ND, npd - at);
+                Part pn{i, 0, int(xsrc.size()), cnt};
+                for (int q = at; q < at + cnt; ++q) {
+                    xsrc.push_back(ci[dl[q].second]);
+                    xcoef.push_back(-(v[dl[q].second] * invd[i]));  // node value = +sum e x
+                    pn.lev = std::max(pn.lev, dl[q].first + 1);
+                }
+                lv = std::max(lv, pn.lev + 1);
+                parts.push_back(pn);
+                at += cnt;
+            }
+            rlev[i] = lv;
+            // partial nodes no earlier than two levels before their row: the value
+            // only lives in the ring
+            for (int p = 0; p < P; ++p) parts[pbase + p].lev = std::max(parts[pbase + p].lev, lv - 2);
+        }
+    }
+    const int np = int(parts.size()), nn = n + np;
+    auto node_lev = [&](int id) { return id < n ? rlev[id] : parts[id - n].lev; };
+    // ---- processing order inside each group: (node level, id)
+    std::vector<int> gnstart(K + 1, 0);
+    {
+        std::vector<int> cntg(K, 0);
+        for (int g = 0; g < K; ++g) cntg[g] = gstart[g + 1] - gstart[g];
+        for (const Part& p : parts) ++cntg[gid[p.owner]];
+        for (int g = 0; g < K; ++g) gnstart[g + 1] = gnstart[g] + cntg[g];
+    }
+    std::vector<int> seq(nn), pos(nn);
+    {
+        std::vector<int> fill(gnstart.begin(), gnstart.end() - 1);
+        for (int g = 0; g < K; ++g)
+            for (int t = gstart[g]; t < gstart[g + 1]; ++t) seq[fill[g]++] = row_of_t(t);
+        for (int p = 0; p < np; ++p) seq[fill[gid[parts[p].owner]]++] = n + p;
+        for (int g = 0; g < K; ++g) {
+            int* q = seq.data() + gnstart[g];
+            const int m = gnstart[g + 1] - gnstart[g];
+            std::stable_sort(q, q + m, [&](int a, int b) { return node_lev(a) < node_lev(b); });
+            for (int u = 0; u < m; ++u) pos[q[u]] = u;
+        }
+    }
+    // inputs of a node: f(src row or partial id as node id, coefficient)
+    auto for_inputs = [&](int id, auto&& f) {
+        if (id >= n) {
+            const Part& p = parts[id - n];
+            for (int q = p.first; q < p.first + p.cnt; ++q) f(xsrc[q], xcoef[q]);
+        } else if (xfirst[id] >= 0) {
+            for (int q = xfirst[id]; q < xfirst[id] + xcnt[id]; ++q)
+                f(xsrc[q] >= 0 ? xsrc[q] : n + (-1 - xsrc[q]), xcoef[q]);
+        } else {
+            for (int k = rp[id]; k < rp[id + 1]; ++k)
+                if (is_dep(id, ci[k])) f(ci[k], v[k] * invd[id]);
+        }
+    };
+    auto node_gid = [&](int id) { return gid[id < n ? id : parts[id - n].owner]; };
+    // ---- ring size.  Own-group values live in a ring of W slots indexed by
+    // processing position; a dependency further back than the ring holds (a few
+    // rows reach hundreds of DAG levels back) is a FAR dependency: the row's value
+    // comes back through the group's own importer, from global memory
+    const int WB = lw_wb(ND), SPC = lw_spc(ND), cap = 32 * nw;
+    const int stepb = nw * WB, chb = SPC * stepb;
+    int maxdist = 0, maxlev = 0;
+    for (int g = 0; g < K; ++g) {
+        for (int u = gnstart[g]; u < gnstart[g + 1]; ++u) {
+            const int id = seq[u];
+            for_inputs(id, [&](int src, double) {
+                if (node_gid(src) == g) maxdist = std::max(maxdist, pos[id] - pos[src]);
+            });
+        }
+        for (int u = gnstart[g], u1; u < gnstart[g + 1]; u = u1) {
+            for (u1 = u; u1 < gnstart[g + 1] && node_lev(seq[u1]) == node_lev(seq[u]);) ++u1;
+            maxlev = std::max(maxlev, u1 - u);
+        }
+    }
+    const int margin = std::max(cap, maxlev) + 32;
+    const int wcap = (225 * 1024 - 3 * chb) / 8 >= 8192 + 4096 ? 8192 : 4096;
+    int W = 64, farthr = INT_MAX;
+    while (W < maxdist + margin) W <<= 1;
+    if (W > wcap) {
+        W = wcap;
+        farthr = W - margin;
+        if (farthr < 64) return;
+    }
+    // ---- import lists in CONSUMER order (first step that needs the value): the
+    // previous group's rows and the group's own far rows.  An entry a step needs
+    // has only entries before it that an earlier-or-equal step needs, all of them
+    // produced before that step can run, so the in-order importer cannot deadlock
+    std::vector<int> hidx(n, -1), hown(n, -1), gimp_off(K + 1, 0), imp;
     std::vector<char> exported(n, 0);
-    int hmax = 0, maxdist = 0;
+    int hmax = 0, nfar = 0;
     for (int g = 0; g < K; ++g) {
         gimp_off[g] = int(imp.size());
-        std::vector<int> need;
-        for (int u = gstart[g]; u < gstart[g + 1]; ++u) {
-            const int i = seq[u];
-            for (int k = rp[i]; k < rp[i + 1]; ++k) {
-                const int j = ci[k];
-                if (!is_dep(i, j)) continue;
-                if (gid[j] == g)
-                    maxdist = std::max(maxdist, pos[i] - pos[j]);
-                else if (!exported[j]) {
-                    exported[j] = 1;
-                    need.push_back(j);
+        int cnt = 0;
+        for (int u = gnstart[g]; u < gnstart[g + 1]; ++u) {
+            const int id = seq[u];
+            bool bad = false;
+            for_inputs(id, [&](int src, double) {
+                if (node_gid(src) != g) {
+                    if (hidx[src] < 0) {
+                        hidx[src] = cnt++;
+                        exported[src] = 1;
+                        imp.push_back(src);
+                    }
+                } else if (pos[id] - pos[src] > farthr) {
+                    if (src >= n) {
+                        bad = true;  // (partial nodes sit right before their row: cannot happen)
+                    } else if (hown[src] < 0) {
+                        hown[src] = cnt++;
+                        exported[src] = 1;
+                        imp.push_back(src);
+                        ++nfar;
+                    }
                 }
-            }
+            });
+            if (bad) return;
         }
-        std::sort(need.begin(), need.end(), [&](int x, int y) { return pos[x] < pos[y]; });
-        for (size_t q = 0; q < need.size(); ++q) hidx[need[q]] = int(q);
-        imp.insert(imp.end(), need.begin(), need.end());
-        hmax = std::max(hmax, int(need.size()));
+        hmax = std::max(hmax, cnt);
     }
     gimp_off[K] = int(imp.size());
-    int W = 64;
-    while (W < maxdist + 32) W <<= 1;
+    const int trash_slot = W + 1 + hmax;
+    if (8 * trash_slot >= (1 << kLwOwnBits) || hmax >= (1 << (32 - kLwOwnBits))) return;
     int ns = 0;
-    for (int t = kLsMaxNS; t >= 2; t /= 2)
-        if (ls_smem_bytes(W, hmax, t) <= 225 * 1024) {
+    for (int t : {8, 6, 4, 3, 2})
+        if (t * chb + t * 8 + 64 + (W + 2 + hmax) * 8 <= 225 * 1024) {
             ns = t;
             break;
         }
     if (ns == 0) return;
-    // programs: one dependency class for the whole level (kernel template)
-    int cls = 0;
-    while (ls_nd(cls) < maxnd) ++cls;
-    // variable-width records (k_gs_lsv) for wide levels unless fixed-class forced
-    const bool var0 = rec_mode == 2 || (rec_mode == 0 && maxnd > kLsVarMin);
-    // lane groups: when most rows fit a smaller class (coarse RS levels: 92-95 %
-    // of the rows have <= 8 of up to 15-19 dependencies) the records use that
-    // class and each wider row takes TWO or FOUR lanes (dependencies 0..ND-1,
-    // ND..2ND-1, ..., summed by xor shuffles).  Quads occupy the first lanes of a
-    // step, then pairs, then single rows, so a level still needs one step per 32
-    // lanes; this also replaces the variable-width records on levels whose widest
-    // row has 17-32 dependencies.  MPREC_LS_PAIRS=0: off.
-    const bool pairs_on = [] {  // read per build (tests toggle it)
-        const char* e = getenv("MPREC_LS_PAIRS");
-        return !(e && e[0] == '0');
-    }();
-    bool pair = false;
-    if (pairs_on && rec_mode == 0 && maxnd > 4) {
-        const int cmax = var0 ? 4 : cls;
-        for (int c2 = 1; c2 < cmax && !pair; ++c2) {
-            if (maxnd > 4 * ls_nd(c2)) continue;
-            int wide = 0;
-            for (int i = 0; i < n; ++i) wide += nd[i] > ls_nd(c2) ? 1 : 0;
-            if (wide * 4 < n) {
-                pair = true;
-                cls = c2;
-            }
-        }
-    }
-    const bool var = var0 && !pair;
-    if (var) cls = kLsVar;
-    const int trash_slot = W + 1 + hmax;
-    std::vector<char> prog;
+    // value-area slot of input src of node id in group g
+    auto in_slot = [&](int g, int id, int src) {
+        if (node_gid(src) != g) return W + 1 + hidx[src];
+        if (pos[id] - pos[src] > farthr) return W + 1 + hown[src];
+        return pos[src] & (W - 1);
+    };
+    // ---- steps: a node level's lanes cut into steps of `cap`; groups padded to whole chunks
     std::vector<int2> gch(K);
-    std::vector<long long> coff(n);
     int64_t nchunks = 0, nsteps_total = 0;
     for (int g = 0; g < K; ++g) {
-        gch[g].x = int(nchunks);
-        const int m = gstart[g + 1] - gstart[g];
-        const int* q = seq.data() + gstart[g];
-        int64_t cbase = 0;
-        int off = kLsCH;
-        for (int u = 0; u < m;) {
-            const int L = lev[q[u]];
-            int cnt = 0, nd4 = 1;
-            if (var) {
-                while (u + cnt < m && cnt < 32 && lev[q[u + cnt]] == L) {
-                    const int n4 = std::max(nd4, (nd[q[u + cnt]] + 3) / 4);
-                    if (16 + (cnt + 1) * ls_rsv(n4) > kLsCH - 16) break;
-                    nd4 = n4;
-                    ++cnt;
-                }
-            } else if (!pair) {
-                while (u + cnt < m && cnt < 32 && lev[q[u + cnt]] == L && 16 + (cnt + 1) * ls_rs(cls) <= kLsCH - 16)
-                    ++cnt;
-            }
-            // grouped steps: rows of the level in order until 32 lanes (1, 2 or 4 per row)
-            int npair = 0, nquad = 0, lanes = cnt;
-            std::vector<int> lane_row, lane_half;
-            if (pair) {
-                auto lanes_of = [&](int i) { return nd[i] <= ls_nd(cls) ? 1 : nd[i] <= 2 * ls_nd(cls) ? 2 : 4; };
-                lanes = 0;
-                while (u + cnt < m && lev[q[u + cnt]] == L) {
-                    const int nl = lanes_of(q[u + cnt]);
-                    // (quads first, then pairs: both stay aligned without padding)
-                    if (lanes + nl > 32 || 16 + (lanes + nl) * ls_rs(cls) > kLsCH - 16) break;
-                    lanes += nl;
-                    nquad += nl == 4;
-                    npair += nl == 2;
-                    ++cnt;
-                }
-                // lane layout: quads, then pairs, then single rows
-                for (int want : {4, 2, 1})
-                    for (int r = 0; r < cnt; ++r)
-                        if (lanes_of(q[u + r]) == want)
-                            for (int hh = 0; hh < want; ++hh) {
-                                lane_row.push_back(r);
-                                lane_half.push_back(hh);
-                            }
-                lanes = int(lane_row.size());
-            }
-            const int RS = var ? ls_rsv(nd4) : ls_rs(cls), ND = var ? 4 * nd4 : ls_nd(cls), bytes = 16 + lanes * RS;
-            if (off + bytes > kLsCH) {
-                cbase = nchunks * int64_t(kLsCH);
-                prog.resize(size_t(cbase + kLsCH), 0);
-                ++nchunks;
-                off = 16;
-            }
-            char* base = prog.data() + cbase + off;
-            int need = 0;
-            for (int ln = 0; ln < lanes; ++ln) {
-                const int r = pair ? lane_row[ln] : ln, half = pair ? lane_half[ln] : 0;
-                const int i = q[u + r];
-                char* rec = base + 16 + ln * RS;
-                int* sl0 = reinterpret_cast<int*>(rec);
-                double* cp = reinterpret_cast<double*>(rec + 16);
-                int* rsl = reinterpret_cast<int*>(rec + 24);
-                double* ep0 = reinterpret_cast<double*>(rec + 32);
-                int* sl1 = reinterpret_cast<int*>(rec + 32 + 8 * ND);
-                auto slot = [&](int d) -> int& {
-                    if (d < 4) return sl0[d];
-                    if (var) return reinterpret_cast<int*>(rec + 64 + 48 * (d / 4 - 1))[d % 4];
-                    return sl1[d - 4];
-                };
-                auto coef = [&](int d) -> double& {
-                    if (var && d >= 4) return reinterpret_cast<double*>(rec + 64 + 48 * (d / 4 - 1) + 16)[d % 4];
-                    return ep0[d];
-                };
-                *cp = 0.0;
-                if (half == 0) {  // first lane of the row's group
-                    rsl[0] = i;
-                    rsl[1] = (pos[i] & (W - 1)) | (exported[i] ? kLsExportBit : 0);
-                    coff[i] = (cbase + off + 16 + ln * RS + 16) | (exported[i] ? 1 : 0);
-                } else {  // further lanes of a pair / quad: c' = 0, no store
-                    rsl[0] = -1;
-                    rsl[1] = trash_slot;
-                }
-                for (int d = 0; d < std::max(ND, 4); ++d) {
-                    if (d < ND) coef(d) = 0.0;
-                    if (d < 4 || d < ND) slot(d) = W;
-                }
-                int d = 0, dd = 0;
-                for (int k = rp[i]; k < rp[i + 1]; ++k) {
-                    const int j = ci[k];
-                    if (!is_dep(i, j)) continue;
-                    if (dd++ / ND != half) continue;  // another lane of the row's group
-                    coef(d) = v[k] * invd[i];
-                    if (gid[j] == g) {
-                        slot(d) = pos[j] & (W - 1);
-                    } else {
-                        slot(d) = W + 1 + hidx[j];
-                        need = std::max(need, hidx[j] + 1);
-                    }
-                    ++d;
-                }
-            }
-            const int hdr[4] = {lanes, var ? nd4 : (cls | (npair << 8) | (nquad << 16)), need, bytes};
-            std::memcpy(base, hdr, 16);
-            *reinterpret_cast<int*>(prog.data() + cbase) += 1;
-            off += bytes;
-            u += cnt;
-            ++nsteps_total;
+        int steps = 0;
+        for (int u = gnstart[g], u1; u < gnstart[g + 1]; u = u1) {
+            for (u1 = u; u1 < gnstart[g + 1] && node_lev(seq[u1]) == node_lev(seq[u]);) ++u1;
+            steps += (u1 - u + cap - 1) / cap;
         }
-        gch[g].y = int(nchunks - gch[g].x);
+        const int chunks = (steps + SPC - 1) / SPC;
+        gch[g] = make_int2(int(nchunks), chunks);
+        nchunks += chunks;
+        nsteps_total += steps;
+    }
+    std::vector<char> prog(size_t(nchunks) * size_t(chb), 0);
+    std::vector<long long> coff(n);
+    for (int g = 0; g < K; ++g) {
+        char* gbase = prog.data() + size_t(gch[g].x) * size_t(chb);
+        const int total_steps = gch[g].y * SPC;
+        int step = 0;
+        auto emit_step = [&](int u0, int u1) {  // nodes seq[u0 .. u1) (possibly none: a padding step)
+            char* sbase = gbase + size_t(step) * size_t(stepb);
+            for (int w = 0; w < nw; ++w) {
+                char* wb = sbase + w * WB;
+                int need = 0;
+                for (int ln = 0; ln < 32; ++ln) {
+                    const int u = u0 + w * 32 + ln;
+                    if (u >= u1) break;
+                    const int id = seq[u];
+                    for_inputs(id, [&](int src, double) {
+                        const int sl = in_slot(g, id, src);
+                        if (sl > W) need = std::max(need, sl - W);
+                    });
+                }
+                for (int ln = 0; ln < 32; ++ln) {
+                    const int u = u0 + w * 32 + ln;
+                    double* e = reinterpret_cast<double*>(wb + 16 * ln);  // e[2q], e[2q + 1] at +512 q
+                    char* tail = wb + lw_tail(ND) + 16 * ln;
+                    auto offp = [&](int d) -> unsigned& {
+                        if (ND == 2) return reinterpret_cast<unsigned*>(wb + lw_off(ND) + 8 * ln)[d];
+                        return reinterpret_cast<unsigned*>(wb + lw_off(ND) + 512 * (d / 4) + 16 * ln)[d % 4];
+                    };
+                    auto coef = [&](int d) -> double& { return *(e + (512 / 8) * (d / 2) + (d % 2)); };
+                    for (int d = 0; d < ND; ++d) {
+                        coef(d) = 0.0;
+                        offp(d) = 8u * unsigned(W);
+                    }
+                    *reinterpret_cast<double*>(tail) = 0.0;
+                    int row = -1;
+                    unsigned own = 8u * unsigned(trash_slot);
+                    if (u < u1) {
+                        const int id = seq[u];
+                        own = 8u * unsigned(pos[id] & (W - 1));
+                        if (id < n) {
+                            row = id;
+                            coff[id] = int64_t(tail - prog.data()) | (exported[id] ? 1 : 0);
+                        }
+                        int d = 0;
+                        for_inputs(id, [&](int src, double cf) {
+                            coef(d) = cf;
+                            offp(d) = 8u * unsigned(in_slot(g, id, src));
+                            ++d;
+                        });
+                    }
+                    *reinterpret_cast<int*>(tail + 8) = row;
+                    *reinterpret_cast<unsigned*>(tail + 12) = own | (unsigned(need) << kLwOwnBits);
+                }
+            }
+            ++step;
+        };
+        for (int u = gnstart[g], u1; u < gnstart[g + 1]; u = u1) {
+            for (u1 = u; u1 < gnstart[g + 1] && node_lev(seq[u1]) == node_lev(seq[u]);) ++u1;
+            for (int l0 = u; l0 < u1; l0 += cap) emit_step(l0, std::min(l0 + cap, u1));
+        }
+        while (step < total_steps) emit_step(0, 0);
     }
     std::vector<int2> gimp(K);
     for (int g = 0; g < K; ++g) gimp[g] = make_int2(gimp_off[g], gimp_off[g + 1] - gimp_off[g]);
+    if (getenv("MPREC_LS_TRACE")) {
+        int dmax = 0, d0 = 0;
+        for (int i = 0; i < n; ++i) dmax = std::max(dmax, rlev[i] + 1);
+        (void)d0;
+        fprintf(stderr, "[ls lw] n=%d dir=%d K=%d nw=%d ND=%d maxnd=%d mean nd %.2f partial nodes %d node-DAG depth %d "
+                        "steps %lld W=%d hmax=%d maxlev=%d far rows %d ns=%d\n",
+                n, dir, K, nw, ND, maxnd, double(sumnd) / n, np, dmax, (long long)nsteps_total, W, hmax, maxlev, nfar, ns);
+    }
     out.prog = std::move(prog);
     out.gch = std::move(gch);
     out.gimp = std::move(gimp);
@@ -798,6 +658,9 @@ static void ls_build_host(const std::vector<int>& rp, const std::vector<int>& ci
     out.nd = maxnd;
     out.ns = ns;
     out.cls = cls;
+    out.nw = nw;
+    out.spc = SPC;
+    out.chb = chb;
     out.ok = true;
 }
 
@@ -821,18 +684,20 @@ static void ls_upload(Ctx& c, LsBuilt& b, LsSched& s) {
     s.nd = b.nd;
     s.ns = b.ns;
     s.cls = b.cls;
-    s.smem = ls_smem_bytes(b.W, b.hmax, b.ns);
+    s.nw = b.nw;
+    s.spc = b.spc;
+    s.chb = b.chb;
+    s.smem = b.ns * b.chb + b.ns * 8 + 64 + (b.W + 2 + b.hmax) * 8;
     s.ok = true;
 }
 
 // Host copy of a level: one download serves both sweep directions.
 struct LsHost {
     int n = 0;
-    std::vector<int> rp, ci, levf, levb;
+    std::vector<int> rp, ci;
     std::vector<double> v, invd;
 };
-static void ls_download(Ctx& c, const CsrView& a, const double* invd_dev, const int* glev_f, const int* glev_b,
-                        LsHost& h) {
+static void ls_download(Ctx& c, const CsrView& a, const double* invd_dev, LsHost& h) {
     const int n = a.n;
     h.n = n;
     h.rp.resize(n + 1);
@@ -843,127 +708,61 @@ static void ls_download(Ctx& c, const CsrView& a, const double* invd_dev, const 
     MG_CUDA(cudaMemcpyAsync(h.ci.data(), a.ci, sizeof(int) * a.nnz, cudaMemcpyDeviceToHost, c.s));
     MG_CUDA(cudaMemcpyAsync(h.v.data(), a.v, sizeof(double) * a.nnz, cudaMemcpyDeviceToHost, c.s));
     MG_CUDA(cudaMemcpyAsync(h.invd.data(), invd_dev, sizeof(double) * n, cudaMemcpyDeviceToHost, c.s));
-    if (glev_f) {
-        h.levf.resize(n);
-        MG_CUDA(cudaMemcpyAsync(h.levf.data(), glev_f, sizeof(int) * n, cudaMemcpyDeviceToHost, c.s));
-    }
-    if (glev_b) {
-        h.levb.resize(n);
-        MG_CUDA(cudaMemcpyAsync(h.levb.data(), glev_b, sizeof(int) * n, cudaMemcpyDeviceToHost, c.s));
-    }
     c.sync();
 }
 
-bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd_dev, int dir, const int* glev_dev, int K,
-                    LsSched& s, int rec_mode) {
-    s = LsSched();
-    if (a.n < 64) return false;
-    LsHost h;
-    ls_download(c, a, invd_dev, dir > 0 ? glev_dev : nullptr, dir > 0 ? nullptr : glev_dev, h);
-    LsBuilt b;
-    ls_build_host(h.rp, h.ci, h.v, dir > 0 ? h.levf : h.levb, h.invd, h.n, dir, K, rec_mode, b);
-    ls_upload(c, b, s);
-    s.rec_mode = rec_mode;
-    return s.ok;
-}
-
 // Both directions from one download, the two host builds on two threads.
-bool build_ls_pair(Ctx& c, const CsrView& a, const double* invd_dev, const int* glev_f, const int* glev_b, int K,
-                   int rec_mode, LsSched& f, LsSched& bw) {
+// nd = 0: dependency class from the level, else 2 / 4 / 8.
+bool build_ls_pair(Ctx& c, const CsrView& a, const double* invd_dev, int K, int nw, int nd, LsSched& f, LsSched& bw) {
     f = LsSched();
     bw = LsSched();
     if (a.n < 64) return false;
     LsHost h;
-    ls_download(c, a, invd_dev, glev_f, glev_b, h);
+    ls_download(c, a, invd_dev, h);
     LsBuilt bf, bb;
-    std::thread t([&] { ls_build_host(h.rp, h.ci, h.v, h.levb, h.invd, h.n, -1, K, rec_mode, bb); });
-    ls_build_host(h.rp, h.ci, h.v, h.levf, h.invd, h.n, +1, K, rec_mode, bf);
+    const int ndsel = nd == 2 ? 1 : nd == 4 ? 2 : nd == 8 ? 3 : 0;
+    nw = std::min(std::max(nw, 1), 8);
+    std::thread t([&] { ls_build_lw(h.rp, h.ci, h.v, h.invd, h.n, -1, K, nw, ndsel, bb); });
+    ls_build_lw(h.rp, h.ci, h.v, h.invd, h.n, +1, K, nw, ndsel, bf);
     t.join();
     if (!bf.ok || !bb.ok) return false;
     ls_upload(c, bf, f);
     ls_upload(c, bb, bw);
-    f.rec_mode = bw.rec_mode = rec_mode;
     return true;
 }
 
-long long* g_ls_stats = nullptr;  // diagnostics: per-group {start, end, wait ns, waits}
+long long* g_ls_stats = nullptr;  // diagnostics: per-group {start, end, first chunk ns, steps}
 
-template <int ND>
-static void launch_ls(Ctx& c, const LsSched& s, double* xnew) {
+template <int ND, bool MULTI>
+static void launch_lw(Ctx& c, const LsSched& s, double* xnew) {
     static bool attr = false;
-    static int max_clusters = -1;
     if (!attr) {
-        MG_CUDA(cudaFuncSetAttribute(k_gs_ls<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+        MG_CUDA(cudaFuncSetAttribute(k_gs_lw<ND, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
         attr = true;
     }
-    // clusters of two thread blocks (DSMEM push across every other group boundary)
-    // when all K/2 clusters fit on the device at once.  Opt-in (MPREC_LS_PUSH=1):
-    // measured slower at c5 (level 0: 0.77 vs 0.59 ms; the per-step ballot and
-    // remote store slow the pushing groups more than the halved boundary
-    // latency saves), DESIGN.md §5.1
-    static const bool push_on = [] {
-        const char* e = getenv("MPREC_LS_PUSH");
-        return e && e[0] == '1';
-    }();
-    bool push = push_on && (s.K % 2 == 0);
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    cfg.gridDim = dim3(s.K);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = s.smem;
-    cfg.stream = c.s;
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (push) {
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k_gs_ls<ND>, &cfg) != cudaSuccess) {
-            cudaGetLastError();
-            n = 0;
-        }
-        push = n >= s.K / 2;
-    }
-    if (!push) cfg.numAttrs = 0;
-    MG_CUDA(cudaLaunchKernelEx(&cfg, k_gs_ls<ND>, (const char*)s.prog.p, (const int2*)s.gch.p, (const int*)s.imp.p,
-                               (const int2*)s.gimp.p, xnew, s.W, s.W + 1 + s.hmax, s.ns, g_ls_stats, push ? 1 : 0));
-    (void)max_clusters;
+    k_gs_lw<ND, MULTI><<<s.K, (s.nw + 3) * 32, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, xnew, s.W, s.hmax,
+                                                             s.ns, s.nw, g_ls_stats);
 }
 
 void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
                  bool xold_zero, const LsSched& s) {
     const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 4.0 * a.n + 24.0 * a.n;
-    {
-        Ctx::Scope sc(&c, MPREC_K_GS, bytes);
-        k_ls_pre<<<(a.n + 255) / 256, 256, 0, c.s>>>(a.n, a.rp, a.ci, a.v, a.diag, invd, b, xold_zero ? nullptr : xold,
-                                                    s.dir, s.coff.p, s.prog.p, xnew);
-        check_launch("gs ls pre");
-        switch (s.cls) {
-            case kLsVar: {
-                static bool attr = false;
-                if (!attr) {
-                    MG_CUDA(cudaFuncSetAttribute(k_gs_lsv, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
-                    attr = true;
-                }
-                k_gs_lsv<<<s.K, kThreads, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, xnew, s.W,
-                                                         s.W + 1 + s.hmax, s.ns);
-                break;
-            }
-            case 0: launch_ls<2>(c, s, xnew); break;
-            case 1: launch_ls<4>(c, s, xnew); break;
-            case 2: launch_ls<8>(c, s, xnew); break;
-            case 3: launch_ls<16>(c, s, xnew); break;
-            default: launch_ls<32>(c, s, xnew); break;
-        }
-        check_launch("gs ls sweep");
+    Ctx::Scope sc(&c, MPREC_K_GS, bytes);
+    k_ls_pre<<<(a.n + 255) / 256, 256, 0, c.s>>>(a.n, a.rp, a.ci, a.v, a.diag, invd, b, xold_zero ? nullptr : xold,
+                                                s.dir, s.coff.p, s.prog.p, xnew);
+    check_launch("gs ls pre");
+    const bool multi = s.nw > 1;
+    switch (s.cls) {
+        case 0: multi ? launch_lw<2, true>(c, s, xnew) : launch_lw<2, false>(c, s, xnew); break;
+        case 1: multi ? launch_lw<4, true>(c, s, xnew) : launch_lw<4, false>(c, s, xnew); break;
+        default: multi ? launch_lw<8, true>(c, s, xnew) : launch_lw<8, false>(c, s, xnew); break;
     }
+    check_launch("gs ls sweep");
 }
 
 void gs_level_sweep(Ctx& c, AmgLevel& L, const double* r, const double* xold, double* xnew, int dir, bool zero);
 
-// Diagnostics: build the level-synchronous programs with K groups on level l,
+// Diagnostics: build the level-synchronous programs with K groups (MPREC_GS_LS_NW warps, MPREC_GS_LS_ND class) on level l,
 // time them against the level's current sweep kernel and compare the results.
 // out[0..9] = ms fwd ls, ms bwd ls, ms fwd cur, ms bwd cur, rel err fwd, rel err bwd,
 //             W, hmax, steps fwd, build ok (1/0)
@@ -971,11 +770,11 @@ void gs_ls_experiment(Ctx& c, Amg& amg, int l, int K, int reps, double* out) {
     AmgLevel& L = *amg.lv[l];
     for (int q = 0; q < 10; ++q) out[q] = 0.0;
     LsSched sf, sb;
-    const int rm = getenv("MPREC_LS_REC") ? atoi(getenv("MPREC_LS_REC")) : 0;
-    const bool okf = build_ls_sched(c, L.a, L.invd.p, +1, L.glev_f, K, sf, rm);
-    const bool okb = okf && build_ls_sched(c, L.a, L.invd.p, -1, L.glev_b, K, sb, rm);
-    out[9] = (okf && okb) ? 1.0 : 0.0;
-    if (!okf || !okb) return;
+    const int nw = getenv("MPREC_GS_LS_NW") ? atoi(getenv("MPREC_GS_LS_NW")) : 1;
+    const int nd = getenv("MPREC_GS_LS_ND") ? atoi(getenv("MPREC_GS_LS_ND")) : 0;
+    const bool ok = build_ls_pair(c, L.a, L.invd.p, K, nw, nd, sf, sb);
+    out[9] = ok ? 1.0 : 0.0;
+    if (!ok) return;
     out[6] = sf.W;
     out[7] = sf.hmax;
     out[8] = sf.nsteps + 1e6 * sf.nd + 1e8 * sf.ns;
@@ -1027,7 +826,7 @@ void gs_ls_experiment(Ctx& c, Amg& amg, int l, int K, int reps, double* out) {
         c.sync();
         long long t0 = h[0];
         for (int g = 0; g < sf.K; ++g) t0 = std::min(t0, h[4 * g]);
-        fprintf(stderr, "[ls stats] level n=%d K=%d (group: start end wait_us waits chunks)\n", n, sf.K);
+        fprintf(stderr, "[ls stats] level n=%d K=%d (group: start end first-chunk_us steps chunks)\n", n, sf.K);
         const int every = atoi(getenv("MPREC_LS_STATS")) >= 2 ? 1 : std::max(1, sf.K / 12);
         for (int g = 0; g < sf.K; g += every)
             fprintf(stderr, "  g%3d: %8.1f %8.1f %8.1f %6lld %5d\n", g, (h[4 * g] - t0) * 1e-3, (h[4 * g + 1] - t0) * 1e-3,

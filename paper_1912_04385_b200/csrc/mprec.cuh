@@ -169,29 +169,21 @@ struct AmgParams {
 };
 
 // Level-synchronous pipelined sweep schedule (gs_ls.cu): K groups of
-// consecutive rows, each a stream of program chunks processed by one warp.
-constexpr int kLsCH = 16384;  // program chunk bytes
-constexpr int kLsMaxNS = 8;   // chunks in the shared-memory ring (at most)
-constexpr int kLsClasses = 5; // dependency classes ND = 2, 4, 8, 16, 32
-constexpr int kLsVar = 9;     // class id of variable-width records (k_gs_lsv)
-constexpr int kLsVarMin = 16; // auto mode: variable-width records when a row has more dependencies
+// consecutive rows, each a stream of fixed-size program steps processed by nw
+// compute warps of one thread block.
 struct LsSched {
     bool ok = false;
     int K = 0, W = 0, hmax = 0, dir = 0, nsteps = 0, nchunks = 0, maxdist = 0, smem = 0, nd = 0, ns = 0, cls = 0;
-    DBuf<char> prog;       // K groups' chunks, kLsCH bytes each
+    int nw = 0, spc = 0, chb = 0;  // compute warps per group, steps per chunk, chunk bytes
+    DBuf<char> prog;       // K groups' chunks
     DBuf<int2> gch;        // per group: first chunk, chunk count
-    DBuf<int> imp;         // per group: rows imported from the previous group
+    DBuf<int> imp;         // per group: rows imported (previous group's, own far rows) in consumer order
     DBuf<int2> gimp;       // per group: offset, count into imp
     DBuf<long long> coff;  // per row: byte offset of its c' slot in prog | export bit
-    int rec_mode = 0;      // how it was built (build_ls_sched)
 };
-// rec_mode: 0 auto (variable-width records when a row has > 16 dependencies),
-// 1 fixed class (k_gs_ls<ND>), 2 variable width (k_gs_lsv)
-bool build_ls_sched(Ctx& c, const CsrView& a, const double* invd, int dir, const int* glev, int K, LsSched& s,
-                    int rec_mode = 0);
-// both directions (one download of the level, two host threads)
-bool build_ls_pair(Ctx& c, const CsrView& a, const double* invd, const int* glev_f, const int* glev_b, int K,
-                   int rec_mode, LsSched& fwd, LsSched& bwd);
+// both directions (one download of the level, two host threads); nd = 0: the
+// dependency class is chosen from the level, else 2 / 4 / 8
+bool build_ls_pair(Ctx& c, const CsrView& a, const double* invd, int K, int nw, int nd, LsSched& fwd, LsSched& bwd);
 void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
                  bool xold_zero, const LsSched& s);
 

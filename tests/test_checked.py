@@ -35,8 +35,8 @@ VARIANTS = {
     "default": {},
     "ilu-warp": {"MPREC_ILU_LS": "0"},
     "ilu-ls32": {"MPREC_ILU_LS": "32"},
-    "gs-ls-fixed": {"MPREC_GS_MODE": "ls", "MPREC_GS_LS_K": "8", "MPREC_GS_LS_REC": "1"},
-    "gs-ls-var": {"MPREC_GS_MODE": "ls", "MPREC_GS_LS_K": "8", "MPREC_GS_LS_REC": "2"},
+    "gs-ls-k8": {"MPREC_GS_MODE": "ls", "MPREC_GS_LS_K": "8"},
+    "gs-ls-k1-nw3-nd4": {"MPREC_GS_MODE": "ls", "MPREC_GS_LS_K": "1", "MPREC_GS_LS_NW": "3", "MPREC_GS_LS_ND": "4"},
     "gs-warp": {"MPREC_GS_MODE": "warp"},
 }
 

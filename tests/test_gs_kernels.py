@@ -1,14 +1,14 @@
 """Every Gauss-Seidel sweep kernel against the oracle.
 
 The setup-time rule (amg_cycle.cu: tune_level_sweep) picks, per AMG level, one
-of the dependency-scheduled sweep kernels (level-synchronous programs with
-fixed-class, lane-group or variable-width records; thread-block cluster; warp
-per row); all of them keep the natural-order semantics of sym_gauss_seidel
-(amg.cpp:25-43).  Each is forced here (MPREC_GS_MODE, MPREC_GS_LS_REC,
-MPREC_LS_PAIRS) on config 2, and the preconditioner apply / solve are checked
-against the oracle.
+of the dependency-scheduled sweep kernels (level-synchronous step programs as
+one group or a pipeline of groups, with one or several lockstep warps and a
+dependency class of 2, 4 or 8 per node; thread-block cluster; warp per row);
+all of them keep the natural-order semantics of sym_gauss_seidel
+(amg.cpp:25-43).  Each is forced here (MPREC_GS_MODE, MPREC_GS_LS_K,
+MPREC_GS_LS_NW, MPREC_GS_LS_ND) on config 2, and the preconditioner apply /
+solve are checked against the oracle.
 """
-import os
 
 import numpy as np
 import pytest
@@ -28,18 +28,25 @@ def cfg2():
     return gen.generate(2)
 
 
-@pytest.mark.parametrize("mode", ["warp", "cluster", "ls", "ls-fixed", "ls-var", "ls-push", "ls-nopairs", ""])
+LS_MODES = {
+    # groups, warps per group, dependency class (0: from the level)
+    "ls": ("16", "1", "0"),
+    "ls-k1": ("1", "1", "0"),          # one group: no boundary, far dependencies through the own importer
+    "ls-k1-nw4": ("1", "4", "0"),      # lockstep warps, named barrier per step
+    "ls-k37-nw2": ("37", "2", "0"),
+    "ls-nd4": ("8", "1", "4"),         # rows wider than 4 dependencies become partial-node trees
+    "ls-nd8": ("4", "2", "8"),
+}
+
+
+@pytest.mark.parametrize("mode", ["warp", "cluster", *LS_MODES, ""])
 @pytest.mark.parametrize("method", ["cpr-amg", "cptr3-amg"])
 def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
-    if mode == "ls-push":
-        # level-synchronous programs launched as clusters of two (DSMEM push); the
-        # switch is read once per process, so this case runs in its own interpreter
-        pytest.skip("MPREC_LS_PUSH is read once per process: covered by test_ls_cluster_push_subprocess")
-    if mode.startswith("ls-"):
-        # level-synchronous programs with fixed-class (k_gs_ls<ND>), variable-width
-        # (k_gs_lsv) or -- auto without lane groups -- single-lane records
-        monkeypatch.setenv("MPREC_GS_LS_REC", {"ls-fixed": "1", "ls-var": "2"}.get(mode, "0"))
-        monkeypatch.setenv("MPREC_LS_PAIRS", "0" if mode == "ls-nopairs" else "1")
+    if mode in LS_MODES:
+        k, nw, nd = LS_MODES[mode]
+        monkeypatch.setenv("MPREC_GS_LS_K", k)
+        monkeypatch.setenv("MPREC_GS_LS_NW", nw)
+        monkeypatch.setenv("MPREC_GS_LS_ND", nd)
         mode = "ls"
     monkeypatch.setenv("MPREC_GS_MODE", mode)
     a, b, _ = cfg2
@@ -70,23 +77,3 @@ def test_ilu_level_sync_solve(gpu, orc, cfg2, method, groups, monkeypatch):
     rg, ro = sg.solve(), so.solve()
     assert abs(rg.iterations - ro.iterations) <= 1
     assert rel(rg.x, ro.x) < 1e-6
-
-
-def test_ls_cluster_push_subprocess(tmp_path):
-    """Cluster-push LS programs (MPREC_LS_PUSH=1, read once per process) against the oracle."""
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, sys; sys.path.insert(0, '.');"
-        "from paper_1912_04385_b200 import gen; from paper_1912_04385_b200.api import gpu; import oracle;"
-        "from tests.systems import random_vec;"
-        "a, b, _ = gen.generate(2); r = random_vec(a.dim, 11);"
-        "sg = gpu().system(a).setup('cptr3-amg', b); so = oracle.api().system(a).setup('cptr3-amg', b);"
-        "e = np.linalg.norm(sg.apply(r) - so.apply(r)) / np.linalg.norm(so.apply(r));"
-        "rg, ro = sg.solve(), so.solve(); print(e, rg.iterations, ro.iterations);"
-        "assert e < 1e-10 and abs(rg.iterations - ro.iterations) <= 1"
-    )
-    env = dict(os.environ, MPREC_LS_PUSH="1", MPREC_GS_MODE="ls", MPREC_GS_LS_K="16")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0, out.stdout + out.stderr
