@@ -341,6 +341,403 @@ __global__ void __launch_bounds__(32) k_rs_select(const int* srp, const int* sci
 #undef RS_LAP
 }
 
+// ---------------------------------------------------------------------------
+// Windowed variant of the one-warp greedy.  The selections follow a front (on
+// the c4 / c5 levels 98 % of consecutive C points lie within three grid lines),
+// and every selection made ~10 dependent L2 round trips (~800 cycles each) on
+// the per-point state.  Here the MUTABLE state of a window of WN consecutive
+// points around the front -- mark, lambda, the per-selection increment counters
+// and the bottom bitmap level of every bucket -- lives in shared memory; the
+// window slides with the front (write back, reload: every few thousand
+// selections).  Points outside the window are still served from global memory,
+// so any selection order is handled; the order itself -- highest bucket, lowest
+// index -- and hence the C/F splitting are unchanged.  The read-only strength
+// graph goes through the L1 (ld.global.nc): consecutive selections share its
+// cache lines.
+struct RsWin {
+    int wb, wn;                 // window [wb, wb + wn), wb % 64 == 0
+    unsigned char* lm;          // [WN] lambda
+    unsigned char* st;          // [WN] mark (2 bits) | per-selection increment counter << 2
+    unsigned long long* l0;     // [nbuckets][WN / 64]
+    int w64;                    // WN / 64
+    // shared-space addresses (explicit atom.shared / red.shared: a generic-address
+    // atomic that lands in shared memory costs several hundred cycles)
+    unsigned l0_a, ic_a, s1_a, s2_a, cnt_a;
+};
+
+__device__ __forceinline__ unsigned sm_and32(unsigned a, unsigned v) {
+    unsigned o;
+    asm volatile("atom.shared.and.b32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ unsigned sm_or32(unsigned a, unsigned v) {
+    unsigned o;
+    asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ unsigned sm_add32(unsigned a, unsigned v) {
+    unsigned o;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(a), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ void sm_red_add(unsigned a, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned sm_ld32(unsigned a) {
+    unsigned o;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(o) : "r"(a) : "memory");
+    return o;
+}
+
+__device__ __forceinline__ bool rw_in(const RsWin& w, int x) { return unsigned(x - w.wb) < unsigned(w.wn); }
+
+__device__ __forceinline__ signed char rw_mark(const RsWin& w, const signed char* mark, int x) {
+    return rw_in(w, x) ? (signed char)(((volatile unsigned char*)w.st)[x - w.wb] & 3)
+                       : ((volatile const signed char*)mark)[x];
+}
+// (only between selections' counting phases: the point's counter is zero)
+__device__ __forceinline__ void rw_set_mark(const RsWin& w, signed char* mark, int x, signed char v) {
+    if (rw_in(w, x))
+        ((volatile unsigned char*)w.st)[x - w.wb] = (unsigned char)v;
+    else
+        mark[x] = v;
+}
+__device__ __forceinline__ int rw_lam(const RsWin& w, const int* lam, int x) {
+    return rw_in(w, x) ? int(((volatile unsigned char*)w.lm)[x - w.wb]) : ((volatile const int*)lam)[x];
+}
+__device__ __forceinline__ void rw_set_lam(const RsWin& w, int* lam, int x, int v) {
+    if (rw_in(w, x))
+        ((volatile unsigned char*)w.lm)[x - w.wb] = (unsigned char)v;
+    else
+        lam[x] = v;
+}
+// fetch-and-increment of the per-selection counter of x (old value)
+__device__ __forceinline__ int rw_inc_add(const RsWin& w, int* inc, int x) {
+    if (rw_in(w, x)) {
+        const int o = x - w.wb, sh = 8 * (o & 3);
+        return int((sm_add32(w.ic_a + 4u * unsigned(o >> 2), 4u << sh) >> (sh + 2)) & 0x3fu);
+    }
+    return atomicAdd(inc + x, 1);
+}
+// read and clear
+__device__ __forceinline__ int rw_inc_take(const RsWin& w, int* inc, int x) {
+    if (rw_in(w, x)) {
+        const int o = x - w.wb, sh = 8 * (o & 3);
+        return int((sm_and32(w.ic_a + 4u * unsigned(o >> 2), ~(0xfcu << sh)) >> (sh + 2)) & 0x3fu);
+    }
+    const int v = ((volatile int*)inc)[x];
+    inc[x] = 0;
+    return v;
+}
+// summary levels (shared memory): clear / set the bit of bottom word w0 in bucket b.
+// Idempotent, so a redundant call is harmless.
+__device__ __forceinline__ void rw_sum_clear(const RsWin& w, const Buckets& q, int w0, int b) {
+    const int w1 = w0 >> 6;
+    const unsigned a1 = w.s1_a + 8u * unsigned(b * q.n1 + w1) + 4u * unsigned((w0 >> 5) & 1);
+    const unsigned n1 = sm_and32(a1, ~(1u << (w0 & 31))) & ~(1u << (w0 & 31));
+    if (n1 == 0u && sm_ld32(a1 ^ 4u) == 0u)
+        sm_and32(w.s2_a + 8u * unsigned(b * q.n2 + (w1 >> 6)) + 4u * unsigned((w1 >> 5) & 1), ~(1u << (w1 & 31)));
+}
+__device__ __forceinline__ void rw_sum_set(const RsWin& w, const Buckets& q, int w0, int b) {
+    const int w1 = w0 >> 6;
+    const unsigned a1 = w.s1_a + 8u * unsigned(b * q.n1 + w1) + 4u * unsigned((w0 >> 5) & 1);
+    if (sm_or32(a1, 1u << (w0 & 31)) == 0u)
+        sm_or32(w.s2_a + 8u * unsigned(b * q.n2 + (w1 >> 6)) + 4u * unsigned((w1 >> 5) & 1), 1u << (w1 & 31));
+}
+__device__ __forceinline__ void rw_remove(const RsWin& w, const Buckets& q, int i, int b) {
+    const int w0 = i >> 6;
+    if (rw_in(w, i)) {
+        // the 64-bit bottom word as two 32-bit halves: whoever empties a half looks at
+        // the other one (lanes run their atomics before their loads, so at least one
+        // lane sees the word empty)
+        const unsigned a = w.l0_a + 8u * unsigned(b * w.w64 + ((i - w.wb) >> 6)) + 4u * unsigned((i >> 5) & 1);
+        const unsigned bit = 1u << (i & 31);
+        if ((sm_and32(a, ~bit) & ~bit) == 0u && sm_ld32(a ^ 4u) == 0u) rw_sum_clear(w, q, w0, b);
+    } else {
+        const unsigned long long bit = 1ull << (i & 63);
+        const unsigned long long o0 = atomicAnd(q.l0 + (int64_t)b * q.n0 + w0, ~bit);
+        if ((o0 & ~bit) == 0ull) rw_sum_clear(w, q, w0, b);
+    }
+    sm_red_add(w.cnt_a + 4u * unsigned(b), -1);
+}
+__device__ __forceinline__ void rw_insert(const RsWin& w, const Buckets& q, int i, int b) {
+    const int w0 = i >> 6;
+    if (rw_in(w, i)) {
+        const unsigned a = w.l0_a + 8u * unsigned(b * w.w64 + ((i - w.wb) >> 6)) + 4u * unsigned((i >> 5) & 1);
+        if (sm_or32(a, 1u << (i & 31)) == 0u) rw_sum_set(w, q, w0, b);
+    } else {
+        if (atomicOr(q.l0 + (int64_t)b * q.n0 + w0, 1ull << (i & 63)) == 0ull) rw_sum_set(w, q, w0, b);
+    }
+    sm_red_add(w.cnt_a + 4u * unsigned(b), 1);
+}
+
+// Window move, all kRsWinThreads threads of the block (the helper warps sleep on a
+// named barrier between moves): write the old window back, then load the new one.
+constexpr int kRsWinThreads = 256;
+__device__ __forceinline__ void rw_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRsWinThreads) : "memory"); }
+
+__device__ void rw_move(unsigned char* st, unsigned char* lm, unsigned long long* wl0, int w64, const Buckets& q,
+                        signed char* mark, int* lam, int n, int WN, int nbuckets, int owb, int own, int nwb, int tid) {
+    // ---- flush [owb, owb + own)
+    if (own > 0) {
+        const int own4 = own & ~3;
+        for (int t = 4 * tid; t < own4; t += 4 * kRsWinThreads) {
+            const unsigned s4 = *reinterpret_cast<const unsigned*>(st + t), l4 = *reinterpret_cast<const unsigned*>(lm + t);
+            *reinterpret_cast<unsigned*>(mark + owb + t) = s4 & 0x03030303u;
+            *reinterpret_cast<int4*>(lam + owb + t) =
+                make_int4(int(l4 & 0xffu), int((l4 >> 8) & 0xffu), int((l4 >> 16) & 0xffu), int(l4 >> 24));
+        }
+        for (int t = own4 + tid; t < own; t += kRsWinThreads) {
+            mark[owb + t] = (signed char)(st[t] & 3);
+            lam[owb + t] = int(lm[t]);
+        }
+        const int words = (own + 63) >> 6;
+        for (int t = tid; t < nbuckets * words; t += kRsWinThreads) {
+            const int b = t / words, x = t - b * words;
+            q.l0[(int64_t)b * q.n0 + (owb >> 6) + x] = wl0[b * w64 + x];
+        }
+        __threadfence();
+    }
+    rw_bar(3);
+    // ---- load [nwb, nwb + nwn)
+    if (nwb >= 0) {
+        const int nwn = min(WN, n - nwb), nwn4 = nwn & ~3;
+        for (int t = 4 * tid; t < nwn4; t += 4 * kRsWinThreads) {
+            const unsigned m4 = *reinterpret_cast<volatile const unsigned*>(mark + nwb + t);
+            const volatile int* lp = lam + nwb + t;
+            const int l0v = lp[0], l1v = lp[1], l2v = lp[2], l3v = lp[3];
+            *reinterpret_cast<unsigned*>(st + t) = m4;
+            *reinterpret_cast<unsigned*>(lm + t) =
+                unsigned(l0v & 0xff) | (unsigned(l1v & 0xff) << 8) | (unsigned(l2v & 0xff) << 16) | (unsigned(l3v & 0xff) << 24);
+        }
+        for (int t = nwn4 + tid; t < nwn; t += kRsWinThreads) {
+            st[t] = (unsigned char)((volatile const signed char*)mark)[nwb + t];
+            lm[t] = (unsigned char)((volatile const int*)lam)[nwb + t];
+        }
+        const int words = (nwn + 63) >> 6;
+        for (int t = tid; t < nbuckets * words; t += kRsWinThreads) {
+            const int b = t / words, x = t - b * words;
+            wl0[b * w64 + x] = ((volatile const unsigned long long*)q.l0)[(int64_t)b * q.n0 + (nwb >> 6) + x];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kRsWinThreads) k_rs_select_win(const int* __restrict__ srp, const int* __restrict__ sci,
+                                                      const int* __restrict__ strp, const int* __restrict__ stci,
+                                                      signed char* mark, int* lam, Buckets q, int nbuckets, int* inc,
+                                                      int* jlist, int* klist, int n, int WN, long long* prof) {
+    extern __shared__ unsigned long long bq_sm[];
+    long long pf[6] = {0, 0, 0, 0, 0, 0}, tp = clock64(), iters = 0, slides = 0, outside = 0;
+#define RS_LAP(k)                          \
+    if (prof) {                            \
+        const long long tn = clock64();    \
+        pf[k] += tn - tp;                  \
+        tp = tn;                           \
+    }
+    const int lane = threadIdx.x & 31, tid = threadIdx.x;
+    __shared__ int nj_sh, nk_sh;
+    __shared__ int cmd[3];  // window move: old base, old size, new base (-1: none, the kernel ends)
+    __shared__ int js0[kRsList], js1[kRsList], kid[kRsList], klam[kRsList];
+    // shared memory: summary levels + counts (as k_rs_select<true>), then the window
+    unsigned long long* s1 = bq_sm;
+    unsigned long long* s2 = s1 + (size_t)nbuckets * q.n1;
+    unsigned long long* wl0 = s2 + (size_t)nbuckets * q.n2;
+    int* sc = reinterpret_cast<int*>(wl0 + (size_t)nbuckets * (WN / 64));
+    unsigned char* wst = reinterpret_cast<unsigned char*>(sc + ((nbuckets + 3) & ~3));
+    unsigned char* wlm = wst + WN;
+    for (int t = tid; t < nbuckets * q.n1; t += kRsWinThreads) s1[t] = q.l1[t];
+    for (int t = tid; t < nbuckets * q.n2; t += kRsWinThreads) s2[t] = q.l2[t];
+    for (int t = tid; t < nbuckets; t += kRsWinThreads) sc[t] = q.cnt[t];
+    q.l1 = s1;
+    q.l2 = s2;
+    q.cnt = sc;
+    rw_move(wst, wlm, wl0, WN / 64, q, mark, lam, n, WN, nbuckets, 0, 0, 0, tid);
+    __syncthreads();
+    if (tid >= 32) {  // helper warps: asleep on barrier 1 until the selecting warp moves the window
+        for (;;) {
+            rw_bar(1);
+            const int owb = ((volatile int*)cmd)[0], own = ((volatile int*)cmd)[1], nwb = ((volatile int*)cmd)[2];
+            rw_move(wst, wlm, wl0, WN / 64, q, mark, lam, n, WN, nbuckets, owb, own, nwb, tid);
+            rw_bar(2);
+            if (nwb < 0) return;
+        }
+    }
+    RsWin w;
+    w.st = wst;
+    w.lm = wlm;
+    w.l0 = wl0;
+    w.w64 = WN / 64;
+    w.l0_a = (unsigned)__cvta_generic_to_shared(wl0);
+    w.ic_a = (unsigned)__cvta_generic_to_shared(wst);
+    w.s1_a = (unsigned)__cvta_generic_to_shared(s1);
+    w.s2_a = (unsigned)__cvta_generic_to_shared(s2);
+    w.cnt_a = (unsigned)__cvta_generic_to_shared(sc);
+    w.wb = 0;
+    w.wn = min(WN, n);
+    auto move_window = [&](int nwb) {  // all lanes of the selecting warp
+        __syncwarp();
+        if (lane == 0) {
+            cmd[0] = w.wb;
+            cmd[1] = w.wn;
+            cmd[2] = nwb;
+        }
+        __syncwarp();
+        rw_bar(1);
+        rw_move(wst, wlm, wl0, WN / 64, q, mark, lam, n, WN, nbuckets, w.wb, w.wn, nwb, tid);
+        rw_bar(2);
+        if (nwb >= 0) {
+            w.wb = nwb;
+            w.wn = min(WN, n - nwb);
+        }
+    };
+    // the window keeps 5/8 of its points behind the selection when it moves (the
+    // selections of the c5 levels hop between ~6 grid lines around a front) and
+    // moves when the selection reaches its last 1/20, or lies outside 16 times
+    // in a row (isolated far selections are served from global memory)
+    const int back = (WN / 8) * 5;
+    int hi = nbuckets - 1, miss = 0;
+    for (;;) {
+        // highest non-empty bucket
+        for (;;) {
+            const int b = hi - lane;
+            const bool ne = b >= 0 && ((volatile int*)q.cnt)[b] > 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, ne);
+            if (bal) {
+                hi -= __ffs(bal) - 1;
+                break;
+            }
+            hi -= 32;
+            if (hi < 0) break;
+        }
+        if (hi < 0) break;
+        ++iters;
+        // lowest index in bucket hi: first non-zero top-level word
+        int first = 0x7fffffff;
+        for (int t = lane; t < q.n2; t += 32)
+            if (((volatile unsigned long long*)q.l2)[(int64_t)hi * q.n2 + t] != 0ull) {
+                first = t;
+                break;
+            }
+        for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+        int i = 0;
+        if (lane == 0) {
+            const unsigned long long x2 = ((volatile unsigned long long*)q.l2)[(int64_t)hi * q.n2 + first];
+            const int w1 = first * 64 + __ffsll((long long)x2) - 1;
+            const unsigned long long x1 = ((volatile unsigned long long*)q.l1)[(int64_t)hi * q.n1 + w1];
+            const int w0 = w1 * 64 + __ffsll((long long)x1) - 1;
+            const unsigned long long x0 =
+                rw_in(w, w0 * 64) ? ((volatile unsigned long long*)w.l0)[hi * w.w64 + ((w0 * 64 - w.wb) >> 6)]
+                                  : ((volatile unsigned long long*)q.l0)[(int64_t)hi * q.n0 + w0];
+            i = w0 * 64 + __ffsll((long long)x0) - 1;
+        }
+        i = __shfl_sync(0xffffffffu, i, 0);
+        // move the window with the front: when the selection runs into the last
+        // quarter, or lies outside twice in a row (an isolated far selection is
+        // served from global memory)
+        {
+            const bool in = rw_in(w, i);
+            const bool tail = in && i - w.wb > WN - WN / 20 && w.wb + WN < n;
+            miss = in ? 0 : miss + 1;
+            if (!in) ++outside;
+            if (tail || miss >= 16) {
+                move_window(max(0, (i - back) & ~63));
+                miss = 0;
+                ++slides;
+            }
+        }
+        if (lane == 0) {
+            rw_set_mark(w, mark, i, kC);
+            rw_remove(w, q, i, hi);
+            nj_sh = 0;
+            nk_sh = 0;
+        }
+        __syncwarp();
+        RS_LAP(0)
+        // phase d: undecided j in S^T_i become F
+        {
+            const int a0 = __ldg(strp + i), a1 = __ldg(strp + i + 1);
+            for (int jj = a0 + lane; jj < a1; jj += 32) {
+                const int j = __ldg(stci + jj);
+                const signed char mj = rw_mark(w, mark, j);
+                if (mj == kU) {
+                    const int lj = rw_lam(w, lam, j), s0 = __ldg(srp + j), s1e = __ldg(srp + j + 1);
+                    rw_set_mark(w, mark, j, kF);
+                    rw_remove(w, q, j, lj);
+                    const int t = atomicAdd(&nj_sh, 1);
+                    if (t < kRsList) {
+                        js0[t] = s0;
+                        js1[t] = s1e;
+                    } else {
+                        jlist[2 * (t - kRsList)] = s0;
+                        jlist[2 * (t - kRsList) + 1] = s1e;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        RS_LAP(1)
+        const int nj = ((volatile int*)&nj_sh)[0];
+        // phase e1: count the increments of every undecided k in S_j; 4 rows at a
+        // time, 8 lanes per row
+        {
+            const int grp = lane >> 3, sub = lane & 7;
+            for (int t0 = 0; t0 < nj; t0 += 4) {
+                const int t = t0 + grp;
+                if (t < nj) {
+                    const int s0 = t < kRsList ? js0[t] : jlist[2 * (t - kRsList)];
+                    const int s1e = t < kRsList ? js1[t] : jlist[2 * (t - kRsList) + 1];
+                    for (int kk = s0 + sub; kk < s1e; kk += 8) {
+                        const int k = __ldg(sci + kk);
+                        if (rw_mark(w, mark, k) == kU && rw_inc_add(w, inc, k) == 0) {
+                            const int lk = rw_lam(w, lam, k);
+                            const int u = atomicAdd(&nk_sh, 1);
+                            if (u < kRsList) {
+                                kid[u] = k;
+                                klam[u] = lk;
+                            } else {
+                                klist[2 * (u - kRsList)] = k;
+                                klist[2 * (u - kRsList) + 1] = lk;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        RS_LAP(2)
+        const int nk = ((volatile int*)&nk_sh)[0];
+        // phase e2: removals (all), then insertions at the incremented lambda; a
+        // removal and an insertion may share a bitmap word, hence two phases
+        for (int t = lane; t < nk; t += 32) {
+            const int k = t < kRsList ? kid[t] : klist[2 * (t - kRsList)];
+            const int lk = t < kRsList ? klam[t] : klist[2 * (t - kRsList) + 1];
+            rw_remove(w, q, k, lk);
+        }
+        __syncwarp();
+        RS_LAP(3)
+        int mx = -1;
+        for (int t = lane; t < nk; t += 32) {
+            const int k = t < kRsList ? kid[t] : klist[2 * (t - kRsList)];
+            const int lk = t < kRsList ? klam[t] : klist[2 * (t - kRsList) + 1];
+            const int nl = lk + rw_inc_take(w, inc, k);
+            rw_set_lam(w, lam, k, nl);
+            rw_insert(w, q, k, nl);
+            mx = max(mx, nl);
+        }
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        hi = max(hi, mx);
+        __syncwarp();
+        RS_LAP(4)
+    }
+    move_window(-1);  // write back; the helper warps leave
+    if (prof && lane == 0) {
+        for (int k = 0; k < 6; ++k) prof[k] = pf[k];
+        prof[6] = iters;
+        prof[7] = slides * 1000000ll + outside;
+    }
+#undef RS_LAP
+}
+
 // --------------------------------------------- RS second and third passes --
 __device__ __forceinline__ bool in_row(const int* sci, int a, int b, int key) {
     while (a < b) {
@@ -874,7 +1271,33 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
         const size_t smem = sizeof(unsigned long long) * (size_t)nbuckets * (q.n1 + q.n2) + sizeof(int) * nbuckets;
         DBuf<long long> prof;
         if (trace_on()) prof.alloc(8);
-        if (smem <= 200 * 1024) {
+        // windowed kernel: summary levels + a window of WN points' state in shared memory
+        static const bool win_on = [] {
+            const char* e = getenv("MPREC_RS_WINDOW");
+            return !(e && e[0] == '0');
+        }();
+        int WN = 0;
+        size_t wsmem = 0;
+        if (win_on && nbuckets <= 127) {  // (increment counters: 6 bits)
+            const size_t fixed = sizeof(unsigned long long) * (size_t)nbuckets * (q.n1 + q.n2) + 4 * (size_t)((nbuckets + 3) & ~3);
+            const size_t budget = 208 * 1024;
+            for (int t = 32768; t >= 2048 && !WN; t >>= 1) {
+                const size_t need = fixed + (size_t)nbuckets * (t / 64) * 8 + 2 * (size_t)t;
+                if (need <= budget) {
+                    WN = t;
+                    wsmem = need;
+                }
+            }
+        }
+        if (WN) {
+            static bool attr = false;
+            if (!attr) {
+                MG_CUDA(cudaFuncSetAttribute(k_rs_select_win, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+                attr = true;
+            }
+            k_rs_select_win<<<1, kRsWinThreads, wsmem, c.s>>>(srp.p, sci.p, strp.p, stci.p, mark, lam.p, q, nbuckets, inc.p, jlist.p,
+                                                   klist.p, n, WN, prof.p);
+        } else if (smem <= 200 * 1024) {
             static bool attr = false;
             if (!attr) {
                 MG_CUDA(cudaFuncSetAttribute(k_rs_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -888,11 +1311,11 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
         }
         check_launch("rs first pass");
         if (trace_on()) {
-            long long h[7];
-            prof.download(h, 7, c.s);
+            long long h[8];
+            prof.download(h, 8, c.s);
             c.sync();
-            fprintf(stderr, "[mprec] rs select n=%d sel=%lld cycles/sel: find %.0f  d %.0f  e1 %.0f  e2a %.0f  e2b %.0f\n", n,
-                    h[6], h[0] / double(h[6]), h[1] / double(h[6]), h[2] / double(h[6]), h[3] / double(h[6]),
+            fprintf(stderr, "[mprec] rs select n=%d sel=%lld window %d (slides %lld, selections outside %lld) cycles/sel: find %.0f  d %.0f  e1 %.0f  e2a %.0f  e2b %.0f\n", n,
+                    h[6], WN, WN ? h[7] / 1000000 : 0ll, WN ? h[7] % 1000000 : 0ll, h[0] / double(h[6]), h[1] / double(h[6]), h[2] / double(h[6]), h[3] / double(h[6]),
                     h[4] / double(h[6]));
         }
     }
