@@ -38,6 +38,7 @@ VARIANTS = {
     "gs-ls-k8": {"MPREC_GS_MODE": "ls", "MPREC_GS_LS_K": "8"},
     "gs-ls-k1-nw3-nd4": {"MPREC_GS_MODE": "ls", "MPREC_GS_LS_K": "1", "MPREC_GS_LS_NW": "3", "MPREC_GS_LS_ND": "4"},
     "gs-warp": {"MPREC_GS_MODE": "warp"},
+    "rs-nowindow": {"MPREC_RS_WINDOW": "0"},  # RS first pass without the shared-memory window: same results
 }
 
 
