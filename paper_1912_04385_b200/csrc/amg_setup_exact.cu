@@ -823,6 +823,131 @@ __global__ void __launch_bounds__(32) k_rs2_seq(const int* srp, const int* sci, 
     }
 }
 
+// Windowed replay of the second pass: the candidates come in increasing index
+// order and every access lies within two rows' reach of the candidate, so the
+// marks (the only mutable state) of a window of kRs2Win points that moves
+// forward with the candidates live in shared memory; accesses outside the window
+// (none on the c5 levels) go to global memory.  Same decisions as k_rs2_seq.
+constexpr int kRs2Win = 128 * 1024, kRs2Threads = 256;
+__device__ __forceinline__ void rs2_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRs2Threads) : "memory"); }
+
+__device__ void rs2_move(unsigned char* wm, signed char* mark, int n, int owb, int own, int nwb, int tid) {
+    if (own > 0) {
+        const int own4 = own & ~3;
+        for (int t = 4 * tid; t < own4; t += 4 * kRs2Threads)
+            *reinterpret_cast<unsigned*>(mark + owb + t) = *reinterpret_cast<const unsigned*>(wm + t);
+        for (int t = own4 + tid; t < own; t += kRs2Threads) mark[owb + t] = (signed char)wm[t];
+        __threadfence();
+    }
+    rs2_bar(3);
+    if (nwb >= 0) {
+        const int nwn = min(kRs2Win, n - nwb), nwn4 = nwn & ~3;
+        for (int t = 4 * tid; t < nwn4; t += 4 * kRs2Threads)
+            *reinterpret_cast<unsigned*>(wm + t) = *reinterpret_cast<volatile const unsigned*>(mark + nwb + t);
+        for (int t = nwn4 + tid; t < nwn; t += kRs2Threads) wm[t] = (unsigned char)((volatile signed char*)mark)[nwb + t];
+    }
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(kRs2Threads) k_rs2_seq_win(const int* __restrict__ srp, const int* __restrict__ sci,
+                                                             signed char* mark, const int* __restrict__ cand, int ncand,
+                                                             int n) {
+    extern __shared__ unsigned char rs2_sm[];
+    unsigned char* wm = rs2_sm;
+    const int lane = threadIdx.x & 31, tid = threadIdx.x;
+    __shared__ int cil[4096];
+    __shared__ int ncil;
+    __shared__ int cmd[3];
+    int wb = max(0, (cand[0] - kRs2Win / 4) & ~63), wn = min(kRs2Win, n - wb);
+    rs2_move(wm, mark, n, 0, 0, wb, tid);
+    __syncthreads();
+    if (tid >= 32) {
+        for (;;) {
+            rs2_bar(1);
+            const int owb = ((volatile int*)cmd)[0], own = ((volatile int*)cmd)[1], nwb = ((volatile int*)cmd)[2];
+            rs2_move(wm, mark, n, owb, own, nwb, tid);
+            rs2_bar(2);
+            if (nwb < 0) return;
+        }
+    }
+    auto move_window = [&](int nwb) {
+        __syncwarp();
+        if (lane == 0) {
+            cmd[0] = wb;
+            cmd[1] = wn;
+            cmd[2] = nwb;
+        }
+        __syncwarp();
+        rs2_bar(1);
+        rs2_move(wm, mark, n, wb, wn, nwb, tid);
+        rs2_bar(2);
+        if (nwb >= 0) {
+            wb = nwb;
+            wn = min(kRs2Win, n - nwb);
+        }
+    };
+    auto get = [&](int x) -> signed char {
+        return unsigned(x - wb) < unsigned(wn) ? (signed char)((volatile unsigned char*)wm)[x - wb]
+                                              : ((volatile signed char*)mark)[x];
+    };
+    auto set_c = [&](int x) {
+        if (unsigned(x - wb) < unsigned(wn))
+            ((volatile unsigned char*)wm)[x - wb] = (unsigned char)kC;
+        else
+            mark[x] = kC;
+    };
+    for (int t = 0; t < ncand; ++t) {
+        const int i = __ldg(cand + t);
+        if (i - wb > kRs2Win - kRs2Win / 4 && wb + kRs2Win < n) move_window(max(0, (i - kRs2Win / 4) & ~63));
+        if (PASS == 3) {  // third pass (k_rs3_seq): an F point with no C among its strong neighbours becomes C
+            bool has_c = false;
+            for (int p = __ldg(srp + i) + lane, pe = __ldg(srp + i + 1); p < pe; p += 32)
+                if (get(__ldg(sci + p)) == kC) has_c = true;
+            has_c = __any_sync(0xffffffffu, has_c);
+            if (!has_c && lane == 0) set_c(i);
+            __syncwarp();
+            continue;
+        }
+        if (get(i) != kF) continue;
+        const int a = __ldg(srp + i), b = __ldg(srp + i + 1);
+        if (lane == 0) ncil = 0;
+        __syncwarp();
+        for (int p = a + lane; p < b; p += 32) {
+            const int j = __ldg(sci + p);
+            if (get(j) == kC) {
+                const int pos = atomicAdd(&ncil, 1);
+                if (pos < 4096) cil[pos] = j;
+            }
+        }
+        __syncwarp();
+        for (int p = a; p < b; ++p) {
+            const int j = __ldg(sci + p);
+            if (get(j) != kF) continue;
+            const int nci = min(((volatile int*)&ncil)[0], 4096);
+            bool shared = false;
+            const int ja = __ldg(srp + j), jb = __ldg(srp + j + 1);
+            for (int kk = ja + lane; kk < jb && !shared; kk += 32) {
+                const int k = __ldg(sci + kk);
+                for (int e = 0; e < nci; ++e)
+                    if (((volatile int*)cil)[e] == k) {
+                        shared = true;
+                        break;
+                    }
+            }
+            shared = __any_sync(0xffffffffu, shared);
+            if (!shared && lane == 0) {
+                set_c(j);
+                const int pos = ncil;
+                if (pos < 4096) cil[pos] = j;
+                ncil = pos + 1;
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+    }
+    move_window(-1);
+}
+
 __global__ void k_rs3_cand(const int* srp, const int* sci, const signed char* mark, int n, int* flag) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1326,7 +1451,21 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
     int ncand = scan(c, s, flag.p, fpos.p, n);
     if (ncand) {
         k_compact<<<nblk(n), 256, 0, c.s>>>(flag.p, fpos.p, n, list.p);
-        k_rs2_seq<<<1, 32, 0, c.s>>>(srp.p, sci.p, mark, list.p, ncand);
+        static const bool win2_on = [] {
+            const char* e = getenv("MPREC_RS_WINDOW");
+            return !(e && e[0] == '0');
+        }();
+        if (win2_on) {
+            static bool attr = false;
+            if (!attr) {
+                MG_CUDA(cudaFuncSetAttribute(k_rs2_seq_win<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRs2Win));
+                MG_CUDA(cudaFuncSetAttribute(k_rs2_seq_win<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRs2Win));
+                attr = true;
+            }
+            k_rs2_seq_win<2><<<1, kRs2Threads, kRs2Win, c.s>>>(srp.p, sci.p, mark, list.p, ncand, n);
+        } else {
+            k_rs2_seq<<<1, 32, 0, c.s>>>(srp.p, sci.p, mark, list.p, ncand);
+        }
         check_launch("rs second pass");
     }
     // ---- third pass
@@ -1334,7 +1473,20 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
     ncand = scan(c, s, flag.p, fpos.p, n);
     if (ncand) {
         k_compact<<<nblk(n), 256, 0, c.s>>>(flag.p, fpos.p, n, list.p);
-        k_rs3_seq<<<1, 32, 0, c.s>>>(srp.p, sci.p, mark, list.p, ncand);
+        static const bool win3_on = [] {
+            const char* e = getenv("MPREC_RS_WINDOW");
+            return !(e && e[0] == '0');
+        }();
+        if (win3_on) {
+            static bool attr3 = false;
+            if (!attr3) {
+                MG_CUDA(cudaFuncSetAttribute(k_rs2_seq_win<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRs2Win));
+                attr3 = true;
+            }
+            k_rs2_seq_win<3><<<1, kRs2Threads, kRs2Win, c.s>>>(srp.p, sci.p, mark, list.p, ncand, n);
+        } else {
+            k_rs3_seq<<<1, 32, 0, c.s>>>(srp.p, sci.p, mark, list.p, ncand);
+        }
         check_launch("rs third pass");
     }
     // ---- coarse ids + direct interpolation

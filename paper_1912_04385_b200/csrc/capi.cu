@@ -624,6 +624,28 @@ int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params
         if (want_T && want_P) {
             h->pat.ensure_sched(c);  // shared, read-only from here on
             c.sync();
+            // keep freed blocks in the stream-ordered pool while the two hierarchies are
+            // built: with the default release threshold (0) every stream
+            // synchronisation returns them to the driver and the next
+            // cudaMallocAsync maps fresh memory, which waits for the other
+            // thread's multi-second first-pass kernel; trimmed again afterwards
+            struct PoolKeep {
+                cudaMemPool_t pool = nullptr;
+                PoolKeep() {
+                    int dev = 0;
+                    cudaGetDevice(&dev);
+                    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) pool = nullptr;
+                    unsigned long long thr = ~0ull;
+                    if (pool) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                }
+                ~PoolKeep() {
+                    unsigned long long thr = 0;
+                    if (pool) {
+                        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+                        cudaMemPoolTrimTo(pool, 0);
+                    }
+                }
+            } pool_keep;
             Ctx c2;
             std::exception_ptr err_T;
             std::thread th([&] {
