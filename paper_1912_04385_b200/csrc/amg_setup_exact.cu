@@ -1578,38 +1578,45 @@ void Amg::setup(Ctx& c, const CsrView& a0, const AmgParams& p, Pattern* pat) {
     // level are built on a helper thread with its own stream as soon as the level
     // is known not to be the coarsest, i.e. while the single-warp RS first pass of
     // the next level runs on this thread's stream (they only read the level).
-    Ctx cs;
+    // (two helpers, each with its own stream: the coarse levels arrive faster than
+    // one thread compiles their programs, and the backlog would end the setup)
+    constexpr int kHelpers = 2;
+    Ctx cs[kHelpers];
     std::mutex qm;
     std::condition_variable qcv;
     std::deque<std::pair<AmgLevel*, bool>> queue;  // (level, is level 0)
     bool qdone = false;
     std::exception_ptr qerr;
-    std::thread helper([&] {
-        StreamAllocScope alloc_on(cs.s);
-        try {
-            for (;;) {
-                std::pair<AmgLevel*, bool> job;
-                {
-                    std::unique_lock<std::mutex> lk(qm);
-                    qcv.wait(lk, [&] { return qdone || !queue.empty(); });
-                    if (queue.empty()) break;
-                    job = queue.front();
-                    queue.pop_front();
+    std::thread helpers[kHelpers];
+    for (int hq = 0; hq < kHelpers; ++hq)
+        helpers[hq] = std::thread([&, hq] {
+            StreamAllocScope alloc_on(cs[hq].s);
+            try {
+                for (;;) {
+                    std::pair<AmgLevel*, bool> job;
+                    {
+                        std::unique_lock<std::mutex> lk(qm);
+                        qcv.wait(lk, [&] { return qdone || !queue.empty(); });
+                        if (queue.empty()) break;
+                        job = queue.front();
+                        queue.pop_front();
+                    }
+                    build_level_schedules(cs[hq], *job.first, job.second ? pat : nullptr);
                 }
-                build_level_schedules(cs, *job.first, job.second ? pat : nullptr);
+                cs[hq].sync();
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(qm);
+                if (!qerr) qerr = std::current_exception();
             }
-            cs.sync();
-        } catch (...) {
-            qerr = std::current_exception();
-        }
-    });
+        });
     auto finish_helper = [&] {
         {
             std::lock_guard<std::mutex> lk(qm);
             qdone = true;
         }
-        qcv.notify_one();
-        if (helper.joinable()) helper.join();
+        qcv.notify_all();
+        for (auto& t : helpers)
+            if (t.joinable()) t.join();
     };
     struct Joiner {  // the helper must not outlive this frame on an exception
         std::function<void()> f;
