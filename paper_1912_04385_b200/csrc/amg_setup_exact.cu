@@ -1405,7 +1405,10 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
         size_t wsmem = 0;
         if (win_on && nbuckets <= 127) {  // (increment counters: 6 bits)
             const size_t fixed = sizeof(unsigned long long) * (size_t)nbuckets * (q.n1 + q.n2) + 4 * (size_t)((nbuckets + 3) & ~3);
-            const size_t budget = 208 * 1024;
+            const size_t budget = [] {  // (MPREC_RS_BUDGET_KB: experiments; more window, less L1 for the strength graph)
+                const char* e = getenv("MPREC_RS_BUDGET_KB");
+                return size_t(e ? atoi(e) : 208) * 1024;
+            }();
             for (int t = 32768; t >= 2048 && !WN; t >>= 1) {
                 const size_t need = fixed + (size_t)nbuckets * (t / 64) * 8 + 2 * (size_t)t;
                 if (need <= budget) {
