@@ -13,10 +13,13 @@ time measured with CUDA events on the library's stream, max over ranks.
 e2e = the same metric through the C ABI `mprec_gpu_solve_system` from HOST
 buffers (H2D of A and b, setup, solve, D2H of x inside the timed region).
 
---impl reference times the reference's CPU path (the oracle restatement:
-the reference itself cannot be built here) on the host cores:
-setup once (untimed), then every step = a bounded sample of 2 GMRES
-iterations of the same system.
+--impl reference times the reference's CPU path on the host cores through the
+oracle restatement (`kind: "port"`): the oracle is pinned bitwise to the
+reference's own sources (oracle/_ref, tests/test_ref_pin.py), but those flatten
+the block matrix to scalar CSR copies (15 GB each at config 5), so
+config 5 runs on the restatement's block storage.  Setup once
+(untimed), then every step = a bounded sample of 2 GMRES iterations of the
+same system.
 
 Multi-GPU: replicas only: every rank solves its own copy of the
 system, no collective on the data path; rank 0 prints the JSON line.
