@@ -498,7 +498,10 @@ static void ls_build_lw(const std::vector<int>& rp, const std::vector<int>& ci, 
         }
     }
     const int margin = std::max(cap, maxlev) + 32;
-    const int wcap = (225 * 1024 - 3 * chb) / 8 >= 8192 + 4096 ? 8192 : 4096;
+    // (MPREC_GS_LS_WCAP: a smaller ring for tests, so that small systems exercise
+    // the far-dependency path)
+    const int wcap_env = getenv("MPREC_GS_LS_WCAP") ? atoi(getenv("MPREC_GS_LS_WCAP")) : 0;
+    const int wcap = wcap_env >= 256 && (wcap_env & (wcap_env - 1)) == 0 ? wcap_env : (225 * 1024 - 3 * chb) / 8 >= 8192 + 4096 ? 8192 : 4096;
     int W = 64, farthr = INT_MAX;
     while (W < maxdist + margin) W <<= 1;
     if (W > wcap) {

@@ -36,6 +36,7 @@ LS_MODES = {
     "ls-k37-nw2": ("37", "2", "0"),
     "ls-nd4": ("8", "1", "4"),         # rows wider than 4 dependencies become partial-node trees
     "ls-nd8": ("4", "2", "8"),
+    "ls-k1-far": ("1", "2", "0"),      # + a 512-slot ring: most dependencies return through the own importer
 }
 
 
@@ -47,6 +48,8 @@ def test_forced_sweep_kernel(gpu, orc, cfg2, mode, method, monkeypatch):
         monkeypatch.setenv("MPREC_GS_LS_K", k)
         monkeypatch.setenv("MPREC_GS_LS_NW", nw)
         monkeypatch.setenv("MPREC_GS_LS_ND", nd)
+        if mode == "ls-k1-far":
+            monkeypatch.setenv("MPREC_GS_LS_WCAP", "512")
         mode = "ls"
     monkeypatch.setenv("MPREC_GS_MODE", mode)
     a, b, _ = cfg2
