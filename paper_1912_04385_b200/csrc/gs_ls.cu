@@ -53,9 +53,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
     asm volatile(
         "{\n .reg .pred p;\n"
@@ -182,13 +179,14 @@ __device__ __forceinline__ void lw_wait(unsigned a, int want, int& have) {
         : "memory");
 }
 
-template <int ND, bool MULTI>
-__global__ void __launch_bounds__(352, 1) k_gs_lw(const char* __restrict__ prog, const int2* __restrict__ gch,
-                                                   const int* __restrict__ imp, const int2* __restrict__ gimp,
-                                                   double* xnew, int W, int hmax, int ns, int nw, long long* stats) {
-    constexpr int WB = lw_wb(ND), SPC = lw_spc(ND);
+template <int ND, int NW>
+__global__ void __launch_bounds__((NW + 3) * 32, 1) k_gs_lw(const char* __restrict__ prog, const int2* __restrict__ gch,
+                                                             const int* __restrict__ imp, const int2* __restrict__ gimp,
+                                                             double* xnew, int W, int hmax, int ns, long long* stats) {
+    constexpr int WB = lw_wb(ND), SPC = lw_spc(ND), nw = NW;
+    constexpr bool MULTI = NW > 1;
     extern __shared__ __align__(128) unsigned char sm[];
-    const int stepb = MULTI ? nw * WB : WB, chb = SPC * stepb;
+    constexpr int stepb = NW * WB, chb = SPC * stepb;
     char* ring = reinterpret_cast<char*>(sm);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + ns * chb);
     int* ctr = reinterpret_cast<int*>(full + ns);  // [0] imported, [1] chunks loaded, [2 + w] chunks consumed by warp w
@@ -279,7 +277,7 @@ __global__ void __launch_bounds__(352, 1) k_gs_lw(const char* __restrict__ prog,
         for (int k = 0; k < SPC; ++k) {
             lw_wait(imp_a, int(R.packed >> kLwOwnBits), have_imp);
             if (MULTI)
-                asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
             else
                 __syncwarp();
             double xv[ND];
@@ -639,9 +637,8 @@ static void ls_build_lw(const std::vector<int>& rp, const std::vector<int>& ci, 
     std::vector<int2> gimp(K);
     for (int g = 0; g < K; ++g) gimp[g] = make_int2(gimp_off[g], gimp_off[g + 1] - gimp_off[g]);
     if (getenv("MPREC_LS_TRACE")) {
-        int dmax = 0, d0 = 0;
+        int dmax = 0;
         for (int i = 0; i < n; ++i) dmax = std::max(dmax, rlev[i] + 1);
-        (void)d0;
         fprintf(stderr, "[ls lw] n=%d dir=%d K=%d nw=%d ND=%d maxnd=%d mean nd %.2f partial nodes %d node-DAG depth %d "
                         "steps %lld W=%d hmax=%d maxlev=%d far rows %d ns=%d\n",
                 n, dir, K, nw, ND, maxnd, double(sumnd) / n, np, dmax, (long long)nsteps_total, W, hmax, maxlev, nfar, ns);
@@ -724,7 +721,7 @@ bool build_ls_pair(Ctx& c, const CsrView& a, const double* invd_dev, int K, int 
     ls_download(c, a, invd_dev, h);
     LsBuilt bf, bb;
     const int ndsel = nd == 2 ? 1 : nd == 4 ? 2 : nd == 8 ? 3 : 0;
-    nw = std::min(std::max(nw, 1), 8);
+    nw = std::min(std::max(nw, 1), 4);  // (kernel instantiations: 1-4 lockstep warps)
     std::thread t([&] { ls_build_lw(h.rp, h.ci, h.v, h.invd, h.n, -1, K, nw, ndsel, bb); });
     ls_build_lw(h.rp, h.ci, h.v, h.invd, h.n, +1, K, nw, ndsel, bf);
     t.join();
@@ -736,15 +733,24 @@ bool build_ls_pair(Ctx& c, const CsrView& a, const double* invd_dev, int K, int 
 
 long long* g_ls_stats = nullptr;  // diagnostics: per-group {start, end, first chunk ns, steps}
 
-template <int ND, bool MULTI>
+template <int ND, int NW>
 static void launch_lw(Ctx& c, const LsSched& s, double* xnew) {
     static bool attr = false;
     if (!attr) {
-        MG_CUDA(cudaFuncSetAttribute(k_gs_lw<ND, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+        MG_CUDA(cudaFuncSetAttribute(k_gs_lw<ND, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
         attr = true;
     }
-    k_gs_lw<ND, MULTI><<<s.K, (s.nw + 3) * 32, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, xnew, s.W, s.hmax,
-                                                             s.ns, s.nw, g_ls_stats);
+    k_gs_lw<ND, NW><<<s.K, (NW + 3) * 32, s.smem, c.s>>>(s.prog.p, s.gch.p, s.imp.p, s.gimp.p, xnew, s.W, s.hmax, s.ns,
+                                                        g_ls_stats);
+}
+template <int ND>
+static void launch_lw_nd(Ctx& c, const LsSched& s, double* xnew) {
+    switch (s.nw) {
+        case 1: launch_lw<ND, 1>(c, s, xnew); break;
+        case 2: launch_lw<ND, 2>(c, s, xnew); break;
+        case 3: launch_lw<ND, 3>(c, s, xnew); break;
+        default: launch_lw<ND, 4>(c, s, xnew); break;
+    }
 }
 
 void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, const double* xold, double* xnew,
@@ -754,11 +760,10 @@ void gs_sweep_ls(Ctx& c, const CsrView& a, const double* invd, const double* b, 
     k_ls_pre<<<(a.n + 255) / 256, 256, 0, c.s>>>(a.n, a.rp, a.ci, a.v, a.diag, invd, b, xold_zero ? nullptr : xold,
                                                 s.dir, s.coff.p, s.prog.p, xnew);
     check_launch("gs ls pre");
-    const bool multi = s.nw > 1;
     switch (s.cls) {
-        case 0: multi ? launch_lw<2, true>(c, s, xnew) : launch_lw<2, false>(c, s, xnew); break;
-        case 1: multi ? launch_lw<4, true>(c, s, xnew) : launch_lw<4, false>(c, s, xnew); break;
-        default: multi ? launch_lw<8, true>(c, s, xnew) : launch_lw<8, false>(c, s, xnew); break;
+        case 0: launch_lw_nd<2>(c, s, xnew); break;
+        case 1: launch_lw_nd<4>(c, s, xnew); break;
+        default: launch_lw_nd<8>(c, s, xnew); break;
     }
     check_launch("gs ls sweep");
 }
