@@ -97,11 +97,11 @@ __global__ void k_ls_pre(int n, const int* __restrict__ rp, const int* __restric
 __host__ __device__ constexpr int ls_nd(int cls) { return 2 << cls; }
 
 // ---------------------------------------------------------------------------
-// Fixed-format warp-steps (k_gs_lw).  Same groups, pipeline and pre-pass as
-// above; what changes is the program format and the step loop.  A lone warp
-// pays ~5-10 cycles per issued instruction, so k_gs_ls's ~120 SASS instructions
-// per step cost 0.2-0.4 us per DAG level; here a step is ~25-45 instructions:
-//   * a step is nw WARP BLOCKS of fixed size (one per compute warp), each an
+// Fixed-format warp-steps (k_gs_lw): the program format and the step loop.  A
+// lone warp pays ~5-10 cycles per issued instruction, so the step loop is kept
+// to ~25-45 instructions (the header-parsed records of the first versions of
+// this file cost ~120 per step, 0.2-0.4 us per DAG level):
+//   * a step is NW WARP BLOCKS of fixed size (one per compute warp), each an
 //     array of 16-byte vectors over the 32 lanes (every load a conflict-free
 //     lane-strided LDS.128): ND/2 vectors of coefficients a_ij / a_ii, one tail
 //     vector {c', row, packed}, ND 32-bit byte offsets of the dependencies in
@@ -111,19 +111,19 @@ __host__ __device__ constexpr int ls_nd(int cls) { return 2 << cls; }
 //     s waits for its dependency values, which are the only loads left on the
 //     step-to-step chain.
 //   * packed = own byte offset in the value area (17 bits) | imports needed (15).
-//   * NODES instead of lane groups: a row with more than ND dependencies becomes
-//     a two-level tree -- partial nodes summing its earliest-available
-//     dependencies (scheduled in earlier steps, in otherwise idle lanes, value
-//     kept in the ring only) and a final node of <= ND inputs.  The node DAG is
-//     re-levelled on the host; no shuffles in the step loop.
+//   * NODES: a row with more than ND dependencies becomes a two-level tree --
+//     partial nodes summing its earliest-available dependencies (scheduled in
+//     earlier steps, in otherwise idle lanes, value kept in the ring only) and a
+//     final node of <= ND inputs.  The node DAG is re-levelled on the host; no
+//     shuffles in the step loop.
 //   * the compute warps never touch an mbarrier: a publisher warp waits for the
 //     bulk copies and advances a `loaded` chunk counter (checked once per
 //     chunk), the compute warps publish `consumed` chunk counters the loader
 //     polls before it refills a ring slot.
-//   * nw > 1 (MULTI): the compute warps run in lockstep, one named barrier per
-//     step (measured slower per step: the warps share the SM's one shared-memory
-//     pipe; kept for levels whose groups would otherwise need several steps per
-//     DAG level).
+//   * NW > 1: the compute warps run in lockstep, one named barrier per step
+//     (slower per step -- the warps share the SM's one shared-memory pipe: 0.108 /
+//     0.135 / 0.185 / 0.243 us for 1-4 warps at ND = 8 -- but one step per DAG
+//     level where a level has up to 32 NW nodes).
 // Padding lanes and padding steps: zero coefficients, the zero slot, row -1,
 // the trash slot.
 __host__ __device__ constexpr int lw_wb(int nd) { return nd == 2 ? 1280 : nd == 4 ? 2048 : 3584; }
