@@ -551,11 +551,13 @@ int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params
         } else {
             h->b_host.assign(b, b + n);
         }
+        auto tr_pre = std::make_unique<Trace>(&c, "setup: rhs upload, operator copy");
         h->b.upload(b, n, c.s);
         h->bbar.ensure(n);
         copy(c, h->bbar.p, h->b.p, n);
         h->abar_val.ensure(nv);
         MG_CUDA(cudaMemcpyAsync(h->abar_val.p, h->a_val.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.s));
+        tr_pre.reset();
         // left_scale (scaling.cpp:149-158)
         {
             Trace tr(&c, "left_scale");
@@ -621,9 +623,26 @@ int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params
             aP = CsrView{nc, nc, h->pat.nnzb, h->pat.rp.p, h->pat.ci.p, h->fP.p, h->pat.dpos.p};
             h->amgP = std::make_unique<Amg>();
         }
+        // ILU(0) of Ā (factors, packed diagonal inverses, solve streams): independent
+        // of the hierarchies, so with two of them it runs on a third thread / stream
+        // meanwhile (its buffers are allocated here, before any concurrency)
+        bool ilu_done = false;
+        auto do_ilu = [&](Ctx& cx) {
+            MG_CUDA(cudaMemcpyAsync(h->lu_val.p, h->abar_val.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, cx.s));
+            h->ilu.lu = view_of(h->pat, h->nb, h->lu_val.p);
+            h->ilu.pat = &h->pat;
+            Trace tr(&cx, "ILU(0) factor");
+            h->ilu.factor(cx);
+            ilu_done = true;
+        };
+        h->lu_val.ensure(nv);
+        if (h->nb == 8) h->ilu.dinv.ensure((size_t)nc * 64);
         if (want_T && want_P) {
-            h->pat.ensure_sched(c);  // shared, read-only from here on
-            c.sync();
+            {
+                Trace tr(&c, "setup: block-pattern sweep schedules");
+                h->pat.ensure_sched(c);  // shared, read-only from here on
+                c.sync();
+            }
             // keep freed blocks in the stream-ordered pool while the two hierarchies are
             // built: with the default release threshold (0) every stream
             // synchronisation returns them to the driver and the next
@@ -640,6 +659,13 @@ int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params
                 }
                 ~PoolKeep() {
                     unsigned long long thr = 0;
+                    const double tt = now_s();
+                    struct Rep {
+                        double t;
+                        ~Rep() {
+                            if (trace_on()) fprintf(stderr, "[mprec] setup: pool trim %34.3f ms\n", (now_s() - t) * 1e3);
+                        }
+                    } rep{tt};
                     if (pool) {
                         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
                         cudaMemPoolTrimTo(pool, 0);
@@ -658,6 +684,17 @@ int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params
                     err_T = std::current_exception();
                 }
             });
+            Ctx c3;
+            std::exception_ptr err_I;
+            std::thread thi([&] {
+                try {
+                    StreamAllocScope alloc_on(c3.s);
+                    do_ilu(c3);
+                    c3.sync();
+                } catch (...) {
+                    err_I = std::current_exception();
+                }
+            });
             std::exception_ptr err_P;
             try {
                 StreamAllocScope alloc_on(c.s);
@@ -668,9 +705,11 @@ int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params
                 err_P = std::current_exception();
             }
             th.join();
+            thi.join();
             // the reference builds C_TT first (stages.cpp:129-138): its error wins
             if (err_T) std::rethrow_exception(err_T);
             if (err_P) std::rethrow_exception(err_P);
+            if (err_I) std::rethrow_exception(err_I);  // (build_cptr3 factors after the hierarchies)
         } else if (want_T) {
             Trace tr(&c, "AMG(C_TT) setup total");
             h->amgT->setup(c, aT, prm, &h->pat);
@@ -678,21 +717,15 @@ int mprec_gpu_setup_opts(mprec_gpu_system* h, int method, const mprec_amg_params
             Trace tr(&c, "AMG(B_PP) setup total");
             h->amgP->setup(c, aP, prm, &h->pat);
         }
-        // ILU(0) of Ā
-        h->lu_val.ensure(nv);
-        MG_CUDA(cudaMemcpyAsync(h->lu_val.p, h->abar_val.p, nv * sizeof(double), cudaMemcpyDeviceToDevice, c.s));
-        h->ilu.lu = view_of(h->pat, h->nb, h->lu_val.p);
-        h->ilu.pat = &h->pat;
-        {
-            Trace tr(&c, "ILU(0) factor");
-            h->ilu.factor(c);
-        }
+        if (!ilu_done) do_ilu(c);
+        if (trace_on()) fprintf(stderr, "[mprec] setup: %.3f s after the hierarchies and ILU\n", now_s() - t0);
         for (DBuf<double>* v : {&h->gT, &h->xT, &h->gP, &h->vP}) v->ensure(nc);
         for (DBuf<double>* v : {&h->z, &h->u, &h->w, &h->x, &h->r, &h->y}) v->ensure(n);
         c.sync();
         h->method = method;
         h->ready = true;
         h->setup_s = now_s() - t0;
+        if (trace_on()) fprintf(stderr, "[mprec] setup: %.3f s total\n", h->setup_s);
     });
 }
 
