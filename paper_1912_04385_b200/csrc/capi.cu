@@ -918,9 +918,13 @@ int mprec_gpu_solve(mprec_gpu_system* h, double tol, int max_iter, double* x, mp
 int mprec_gpu_solve_system(const mprec_bsr* a, const double* b, int method, double tol, int max_iter, double* x,
                            mprec_solve_result* out) {
     mprec_gpu_system* h = nullptr;
+    const double t0 = now_s();
     int st = mprec_gpu_create(a, &h);
+    const double t1 = now_s();
     if (st == MPREC_OK) st = mprec_gpu_setup(h, method, nullptr, b);
+    const double t2 = now_s();
     if (st == MPREC_OK) st = mprec_gpu_solve(h, tol, max_iter, x, out, nullptr, 0);
+    const double t3 = now_s();
     if (h) {
         std::string keep = g_err;
         int kp = g_payload;
@@ -928,6 +932,9 @@ int mprec_gpu_solve_system(const mprec_bsr* a, const double* b, int method, doub
         g_err = keep;
         g_payload = kp;
     }
+    if (trace_on())
+        fprintf(stderr, "[mprec] solve_system: create (validate + H2D) %.3f s, setup %.3f s, solve %.3f s, destroy %.3f s\n",
+                t1 - t0, t2 - t1, t3 - t2, now_s() - t3);
     return st;
 }
 

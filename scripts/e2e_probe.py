@@ -1,6 +1,6 @@
 import ctypes as C, os, sys, time
 import numpy as np
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1912_04385_b200 import gen
 from paper_1912_04385_b200.api import gpu, _Result, _ptr
 api = gpu()
