@@ -1,4 +1,5 @@
-"""Critical-path model of the level-synchronous Gauss-Seidel programs (gs_ls.cu):
+"""Critical-path model of the level-synchronous Gauss-Seidel programs (gs_ls.cu, one
+compute warp per group; written for the first record format, still the model behind DESIGN §5.1):
 K contiguous groups, rows in (DAG level, width, index) order inside a group,
 <= 32 rows per step; a step starts after the group's previous step and after
 every step (of the previous group) it imports from, plus a hop.  Calibrated on
