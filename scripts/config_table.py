@@ -1,6 +1,7 @@
 """Per-config table (BASELINE configs 1-4): GPU vs CPU oracle, both methods where
-BASELINE names two, plus the per-kernel-class time split of the GPU solve
-(CUDA events per launch).  Writes JSON to stdout.
+BASELINE names two, plus the per-kernel-class time split of the GPU solve and
+the per-stage split of one preconditioner application (CUDA events per launch;
+BASELINE config 3 asks for the per-stage kernel time split).  Writes JSON to stdout.
 
     python scripts/config_table.py [cids] [--no-oracle]
 """
@@ -46,6 +47,26 @@ for cid in cids:
             if n.value:
                 split[name] = {"ms": round(tt.value, 3), "launches": n.value,
                                "GBps": round(by.value / max(tt.value, 1e-9) / 1e6, 1)}
+        # per-stage device time of one preconditioner application (Alg. 1/2 stages:
+        # temperature AMG / pressure AMG / ILU(0) for cptr3-amg): kernel time of each
+        # stage applied alone to a fixed vector, mean of 10
+        import numpy as np
+        rv = np.random.default_rng(1).standard_normal(a.dim)
+        stage_ms = []
+        for st in range(s.n_stages()):
+            s.apply_stage(st, rv)  # warm
+            g.call("reset_stats", s.h)
+            g.call("profile", s.h, 1)
+            for _ in range(10):
+                s.apply_stage(st, rv)
+            g.call("profile", s.h, 0)
+            tot = 0.0
+            for k in range(len(KCLASS)):
+                tt, n, by = C.c_double(), C.c_int64(), C.c_double()
+                g.call("kernel_stats", s.h, k, C.byref(tt), C.byref(n), C.byref(by))
+                tot += tt.value
+            stage_ms.append(round(tot / 10, 4))
+        row["gpu_stage_ms"] = stage_ms
         row.update(gpu_iterations=list(r.attempt_iterations), gpu_converged=r.converged,
                    gpu_true_residual=r.final_true_residual, gpu_split=split,
                    gpu_x_err=float(((r.x - xs) ** 2).sum() ** 0.5 / (xs ** 2).sum() ** 0.5))
