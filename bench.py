@@ -234,6 +234,17 @@ def ours(args):
         del aw, bw, xw
         x = np.zeros(a.dim)
         r2 = _Result()
+        # the step's host buffers are page-locked before the timed region (the bench
+        # contract: inputs copied from pinned host memory); the library's plain
+        # cudaMemcpyAsync then runs at PCIe speed instead of staging pageable memory
+        rt = torch.cuda.cudart()
+        pinned = []
+        for arr in (a.row_ptr, a.col_idx, a.values, b, x):
+            try:
+                if int(rt.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)) == 0:
+                    pinned.append(arr)
+            except Exception:
+                pass
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -241,12 +252,15 @@ def ours(args):
         api.call("solve_system", C.byref(a._c), _ptr(b), method_id, args.tol, args.max_iter, _ptr(x), C.byref(r2))
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
+        for arr in pinned:
+            rt.cudaHostUnregister(arr.ctypes.data)
         from paper_1912_04385_b200 import replicas
         el = replicas.reduce_max(el, dev)
         h2d = a.row_ptr.nbytes + a.col_idx.nbytes + a.values.nbytes + b.nbytes
         e2e = {"value": replicas.reduce_sum(r2.total_iterations, dev) / el, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(x.nbytes), "seconds": el, "setup_s": r2.setup_s, "solve_s": r2.solve_s,
                "iterations": r2.total_iterations, "timer": "host wall clock around the synchronous C-ABI call",
+               "host_buffers": "page-locked (cudaHostRegister)" if len(pinned) == 5 else "pageable",
                "warm": "library kernels loaded by an untimed config-2 solve_system call first",
                "x_err_vs_xstar": float(np.linalg.norm(x - xs) / np.linalg.norm(xs))}
         del x
