@@ -188,13 +188,81 @@ void compute_invd(Ctx& c, const CsrView& a, double* invd) {
     check_launch("invd");
 }
 
+// Fused residual + restriction (K15): rc = R (r - A x) in one launch
+// (amg.cpp:224-226).  A coarse row's lanes walk its R entries; each entry's fine
+// residual t_j = r_j - (A x)_j is recomputed on the fly with exactly the
+// association k_csr<LNA> uses for the unfused residual (LNA strided partial sums,
+// xor butterfly), and the R row is summed like k_csr<LNR>: bitwise equal to the
+// two-launch path.  Each fine row is recomputed once per R entry that refers to
+// it (~2x on the RS levels), so it pays only where the level is launch-bound.
+template <int LNA, int LNR>
+__global__ void __launch_bounds__(256) k_resid_restrict(const int* __restrict__ rp, const int* __restrict__ ci,
+                                                        const double* __restrict__ v, const double* __restrict__ x,
+                                                        const double* __restrict__ r, const int* __restrict__ rrp,
+                                                        const int* __restrict__ rci, const double* __restrict__ rv,
+                                                        double* __restrict__ rc, int nc) {
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    const int row = int(g / LNR), s = int(g % LNR);
+    double acc = 0.0;
+    if (row < nc)
+        for (int k = __ldg(rrp + row) + s; k < __ldg(rrp + row + 1); k += LNR) {
+            const int j = __ldg(rci + k);
+            const int a0 = __ldg(rp + j), a1 = __ldg(rp + j + 1);
+            double p[LNA];
+#pragma unroll
+            for (int s2 = 0; s2 < LNA; ++s2) {
+                double ps = 0.0;
+                for (int q = a0 + s2; q < a1; q += LNA) ps += __ldg(v + q) * __ldg(x + __ldg(ci + q));
+                p[s2] = ps;
+            }
+#pragma unroll
+            for (int o = 1; o < LNA; o <<= 1)
+#pragma unroll
+                for (int i = 0; i < LNA; i += 2 * o) p[i] = p[i] + p[i + o];
+            acc += __ldg(rv + k) * (__ldg(r + j) - p[0]);
+        }
+#pragma unroll
+    for (int o = 1; o < LNR; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (row < nc && s == 0) rc[row] = acc;
+}
+
+static int csr_lanes(const CsrView& a) {
+    const double per_row = double(a.nnz) / std::max(a.n, 1);
+    return per_row <= 3.0 ? 2 : per_row <= 6.0 ? 4 : per_row <= 12.0 ? 8 : 16;
+}
+
+template <int LNA>
+static void launch_rr(Ctx& c, const CsrView& a, const CsrView& R, const double* x, const double* r, double* rc, int lnr) {
+    const int grid = int(((int64_t)R.n * lnr + 255) / 256);
+    switch (lnr) {
+        case 2: k_resid_restrict<LNA, 2><<<grid, 256, 0, c.s>>>(a.rp, a.ci, a.v, x, r, R.rp, R.ci, R.v, rc, R.n); break;
+        case 4: k_resid_restrict<LNA, 4><<<grid, 256, 0, c.s>>>(a.rp, a.ci, a.v, x, r, R.rp, R.ci, R.v, rc, R.n); break;
+        case 8: k_resid_restrict<LNA, 8><<<grid, 256, 0, c.s>>>(a.rp, a.ci, a.v, x, r, R.rp, R.ci, R.v, rc, R.n); break;
+        default: k_resid_restrict<LNA, 16><<<grid, 256, 0, c.s>>>(a.rp, a.ci, a.v, x, r, R.rp, R.ci, R.v, rc, R.n); break;
+    }
+}
+
+// rc = R (r - A x)
+void csr_resid_restrict(Ctx& c, const CsrView& a, const CsrView& R, const double* x, const double* r, double* rc) {
+    if (R.n == 0) return;
+    const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 16.0 * a.n + 12.0 * R.nnz + 4.0 * (R.n + 1) + 8.0 * R.n;
+    Ctx::Scope sc(&c, MPREC_K_CSR, bytes);
+    const int lnr = csr_lanes(R);
+    switch (csr_lanes(a)) {
+        case 2: launch_rr<2>(c, a, R, x, r, rc, lnr); break;
+        case 4: launch_rr<4>(c, a, R, x, r, rc, lnr); break;
+        case 8: launch_rr<8>(c, a, R, x, r, rc, lnr); break;
+        default: launch_rr<16>(c, a, R, x, r, rc, lnr); break;
+    }
+    check_launch("resid+restrict");
+}
+
 void csr_spmv(Ctx& c, const CsrView& a, const double* x, double* y, const double* b, bool add_to_y, int kclass) {
     if (a.n == 0) return;
     const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 8.0 * a.m + 8.0 * a.n + ((b || add_to_y) ? 8.0 * a.n : 0.0);
     Ctx::Scope sc(&c, kclass, bytes);
     const int mode = add_to_y ? 2 : (b ? 1 : 0);
-    const double per_row = double(a.nnz) / std::max(a.n, 1);
-    const int ln = per_row <= 3.0 ? 2 : per_row <= 6.0 ? 4 : per_row <= 12.0 ? 8 : 16;
+    const int ln = csr_lanes(a);
     const int64_t threads = (int64_t)a.n * ln;
     const int grid = int((threads + 255) / 256);
     switch (ln) {
@@ -245,9 +313,18 @@ void Amg::cycle(Ctx& c, int l, const double* r, double* x) {
     level_sweep(c, L, r, nullptr, L.xf.p, +1, true);
     if (pend) fill_pending(c, x, n);
     level_sweep(c, L, r, L.xf.p, x, -1, false);
-    // rc = R (r - A x)
-    csr_spmv(c, L.a, x, L.t.p, r, false, MPREC_K_CSR);
-    csr_spmv(c, N.r.view(), L.t.p, N.b.p, nullptr, false, MPREC_K_CSR);
+    // rc = R (r - A x): one fused launch on the launch-bound (small) levels, two
+    // CSR products above (bitwise the same; MPREC_FUSE_RR_MAX = largest fused level)
+    static const int fuse_max = [] {
+        const char* e = getenv("MPREC_FUSE_RR_MAX");
+        return e ? atoi(e) : 100000;
+    }();
+    if (L.n <= fuse_max) {
+        csr_resid_restrict(c, L.a, N.r.view(), x, r, N.b.p);
+    } else {
+        csr_spmv(c, L.a, x, L.t.p, r, false, MPREC_K_CSR);
+        csr_spmv(c, N.r.view(), L.t.p, N.b.p, nullptr, false, MPREC_K_CSR);
+    }
     cycle(c, l + 1, N.b.p, N.x.p);
     // x += P ec
     csr_spmv(c, N.p.view(), N.x.p, x, nullptr, true, MPREC_K_CSR);

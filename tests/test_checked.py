@@ -60,3 +60,13 @@ def test_checked_build(variant):
     ck = _run(VARIANTS[variant], True)
     rg = _run(VARIANTS[variant], False)
     assert ck == rg, (ck, rg)
+
+
+def test_fused_residual_restriction_bitwise():
+    """K15: the fused rc = R (r - A x) kernel (small levels, amg_cycle.cu) reproduces the
+    two-launch path bit for bit: same iteration counts and solution norms with the
+    fusion off (MPREC_FUSE_RR_MAX=0), on for every level, and at the default threshold."""
+    off = _run({"MPREC_FUSE_RR_MAX": "0"}, False)
+    on_all = _run({"MPREC_FUSE_RR_MAX": "2000000000"}, False)
+    dflt = _run({}, False)
+    assert off == on_all == dflt, (off, on_all, dflt)
