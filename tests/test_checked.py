@@ -38,7 +38,8 @@ VARIANTS = {
     "gs-ls-k8": {"MPREC_GS_MODE": "ls", "MPREC_GS_LS_K": "8"},
     "gs-ls-k1-nw3-nd4": {"MPREC_GS_MODE": "ls", "MPREC_GS_LS_K": "1", "MPREC_GS_LS_NW": "3", "MPREC_GS_LS_ND": "4"},
     "gs-warp": {"MPREC_GS_MODE": "warp"},
-    "rs-nowindow": {"MPREC_RS_WINDOW": "0"},  # RS first pass without the shared-memory window: same results
+    "rs-nowindow": {"MPREC_RS_WINDOW": "0"},  # RS passes without their shared-memory windows: same results
+    "rs-small-window": {"MPREC_RS_BUDGET_KB": "24"},  # 4k-point window: it moves, selections fall outside
 }
 
 
@@ -60,6 +61,15 @@ def test_checked_build(variant):
     ck = _run(VARIANTS[variant], True)
     rg = _run(VARIANTS[variant], False)
     assert ck == rg, (ck, rg)
+
+
+def test_rs_window_does_not_change_results():
+    """The windowed RS passes (amg_setup_exact.cu) are an implementation detail: without
+    the windows, and with a window so small that it keeps moving and many selections
+    are served from global memory, setup and solves are bit-for-bit the default's."""
+    dflt = _run({}, False)
+    assert _run(VARIANTS["rs-nowindow"], False) == dflt
+    assert _run(VARIANTS["rs-small-window"], False) == dflt
 
 
 def test_fused_residual_restriction_bitwise():
