@@ -341,6 +341,30 @@ __global__ void __launch_bounds__(32) k_rs_select(const int* srp, const int* sci
 #undef RS_LAP
 }
 
+// Two-hop adjacency records for the windowed first pass.  A selection of point i
+// walks S^T_i and, for every j in it that becomes F, S_j: four dependent loads
+// (row pointer -> column list, twice) at L2 latency.  The record of i holds all of
+// it -- [0] = |S^T_i|, then per j a block {j, |S_j|, S_j padded to maxS} -- in
+// one fixed-size, 128-byte-aligned run (1-4 cache lines, fetched in one round
+// trip right after the selection is known).  Levels whose record would exceed
+// kRsRecMax ints keep the CSR walk.
+constexpr int kRsRecMax = 128;
+__global__ void k_rs_records(const int* __restrict__ srp, const int* __restrict__ sci, const int* __restrict__ strp,
+                             const int* __restrict__ stci, int n, int B, int RW, int* __restrict__ rec) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int* r = rec + (int64_t)RW * i;
+    const int t0 = strp[i], nt = strp[i + 1] - t0;
+    r[0] = nt;
+    for (int t = 0; t < nt; ++t) {
+        const int j = stci[t0 + t], s0 = srp[j], ns = srp[j + 1] - s0;
+        int* blk = r + 1 + t * B;
+        blk[0] = j;
+        blk[1] = ns;
+        for (int u = 0; u < ns; ++u) blk[2 + u] = sci[s0 + u];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Windowed variant of the one-warp greedy.  The selections follow a front (on
 // the c4 / c5 levels 98 % of consecutive C points lie within three grid lines),
@@ -525,7 +549,8 @@ __device__ void rw_move(unsigned char* st, unsigned char* lm, unsigned long long
 __global__ void __launch_bounds__(kRsWinThreads) k_rs_select_win(const int* __restrict__ srp, const int* __restrict__ sci,
                                                       const int* __restrict__ strp, const int* __restrict__ stci,
                                                       signed char* mark, int* lam, Buckets q, int nbuckets, int* inc,
-                                                      int* jlist, int* klist, int n, int WN, long long* prof) {
+                                                      int* jlist, int* klist, int n, int WN, long long* prof,
+                                                      const int* __restrict__ rec, int recB, int recW) {
     extern __shared__ unsigned long long bq_sm[];
     long long pf[6] = {0, 0, 0, 0, 0, 0}, tp = clock64(), iters = 0, slides = 0, outside = 0;
 #define RS_LAP(k)                          \
@@ -538,6 +563,7 @@ __global__ void __launch_bounds__(kRsWinThreads) k_rs_select_win(const int* __re
     __shared__ int nj_sh, nk_sh;
     __shared__ int cmd[3];  // window move: old base, old size, new base (-1: none, the kernel ends)
     __shared__ int js0[kRsList], js1[kRsList], kid[kRsList], klam[kRsList];
+    __shared__ int recs[kRsRecMax], newlist[32];
     // shared memory: summary levels + counts (as k_rs_select<true>), then the window
     unsigned long long* s1 = bq_sm;
     unsigned long long* s2 = s1 + (size_t)nbuckets * q.n1;
@@ -645,6 +671,14 @@ __global__ void __launch_bounds__(kRsWinThreads) k_rs_select_win(const int* __re
                 ++slides;
             }
         }
+        int rw0 = 0, rw1 = 0, rw2 = 0, rw3 = 0;  // the selection's two-hop record (in flight during lane 0's work)
+        if (rec) {
+            const int* rp_ = rec + (int64_t)recW * i + lane;
+            rw0 = __ldg(rp_);
+            if (recW > 32) rw1 = __ldg(rp_ + 32);
+            if (recW > 64) rw2 = __ldg(rp_ + 64);
+            if (recW > 96) rw3 = __ldg(rp_ + 96);
+        }
         if (lane == 0) {
             rw_set_mark(w, mark, i, kC);
             rw_remove(w, q, i, hi);
@@ -653,6 +687,58 @@ __global__ void __launch_bounds__(kRsWinThreads) k_rs_select_win(const int* __re
         }
         __syncwarp();
         RS_LAP(0)
+        if (rec) {
+            recs[lane] = rw0;
+            if (recW > 32) recs[32 + lane] = rw1;
+            if (recW > 64) recs[64 + lane] = rw2;
+            if (recW > 96) recs[96 + lane] = rw3;
+            __syncwarp();
+            // phase d: undecided j in S^T_i become F (one lane per j; |S^T_i| <= 32 here)
+            const int nst = ((volatile int*)recs)[0];
+            bool newf = false;
+            if (lane < nst) {
+                const int j = ((volatile int*)recs)[1 + lane * recB];
+                if (rw_mark(w, mark, j) == kU) {
+                    const int lj = rw_lam(w, lam, j);
+                    rw_set_mark(w, mark, j, kF);
+                    rw_remove(w, q, j, lj);
+                    newf = true;
+                }
+            }
+            const unsigned nm = __ballot_sync(0xffffffffu, newf);
+            if (newf) newlist[__popc(nm & ((1u << lane) - 1))] = lane;
+            const int nnew = __popc(nm);
+            __syncwarp();
+            RS_LAP(1)
+            // phase e1: count the increments of every undecided k in S_j of the new F
+            // points: MS lanes per j (MS = power of two >= maxS), 32 / MS points a round
+            const int maxs = recB - 2;
+            const int ms = maxs <= 4 ? 4 : maxs <= 8 ? 8 : maxs <= 16 ? 16 : 32;
+            const int per = 32 / ms, sub = lane % ms, slot = lane / ms;
+            for (int r0 = 0; r0 < nnew; r0 += per) {
+                const int sidx = r0 + slot;
+                if (sidx < nnew) {
+                    const int t = ((volatile int*)newlist)[sidx];
+                    const int ns = ((volatile int*)recs)[2 + t * recB];
+                    if (sub < ns) {
+                        const int k = ((volatile int*)recs)[3 + t * recB + sub];
+                        if (rw_mark(w, mark, k) == kU && rw_inc_add(w, inc, k) == 0) {
+                            const int lk = rw_lam(w, lam, k);
+                            const int u = atomicAdd(&nk_sh, 1);
+                            if (u < kRsList) {
+                                kid[u] = k;
+                                klam[u] = lk;
+                            } else {
+                                klist[2 * (u - kRsList)] = k;
+                                klist[2 * (u - kRsList) + 1] = lk;
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            RS_LAP(2)
+        } else {
         // phase d: undecided j in S^T_i become F
         {
             const int a0 = __ldg(strp + i), a1 = __ldg(strp + i + 1);
@@ -705,6 +791,7 @@ __global__ void __launch_bounds__(kRsWinThreads) k_rs_select_win(const int* __re
         }
         __syncwarp();
         RS_LAP(2)
+        }
         const int nk = ((volatile int*)&nk_sh)[0];
         // phase e2: removals (all), then insertions at the incremented lambda; a
         // removal and an insertion may share a bitmap word, hence two phases
@@ -1423,8 +1510,30 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
                 MG_CUDA(cudaFuncSetAttribute(k_rs_select_win, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
                 attr = true;
             }
+            // two-hop adjacency records when they fit kRsRecMax ints (levels 0-1 of c5)
+            DBuf<int> rec;
+            int recB = 0, recW = 0;
+            {
+                int smax = 0;
+                DBuf<int> mx2(1);
+                MG_CUDA(cudaMemsetAsync(mx2.p, 0, sizeof(int), c.s));
+                k_max_int<<<std::min(nblk(n), 1024), 256, 0, c.s>>>(scnt.p, n, mx2.p);
+                MG_CUDA(cudaMemcpyAsync(&smax, mx2.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+                c.sync();
+                const int B = 2 + smax, RW = (1 + lmax * B + 31) & ~31;
+                static const bool rec_on = [] {
+                    const char* e = getenv("MPREC_RS_RECORDS");
+                    return !(e && e[0] == '0');
+                }();
+                if (rec_on && RW <= kRsRecMax && lmax <= 32 && smax <= 32) {
+                    recB = B;
+                    recW = RW;
+                    rec.alloc((size_t)RW * n);
+                    k_rs_records<<<nblk(n), 256, 0, c.s>>>(srp.p, sci.p, strp.p, stci.p, n, B, RW, rec.p);
+                }
+            }
             k_rs_select_win<<<1, kRsWinThreads, wsmem, c.s>>>(srp.p, sci.p, strp.p, stci.p, mark, lam.p, q, nbuckets, inc.p, jlist.p,
-                                                   klist.p, n, WN, prof.p);
+                                                   klist.p, n, WN, prof.p, rec.p, recB, recW);
         } else if (smem <= 200 * 1024) {
             static bool attr = false;
             if (!attr) {
