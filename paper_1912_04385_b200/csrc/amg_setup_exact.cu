@@ -637,17 +637,25 @@ __global__ void __launch_bounds__(kRsWinThreads) k_rs_select_win(const int* __re
         }
         if (hi < 0) break;
         ++iters;
-        // lowest index in bucket hi: first non-zero top-level word
+        // lowest index in bucket hi: first non-zero top-level word (one ballot while
+        // the top level has <= 32 words, i.e. up to 8M points), then the descent on
+        // every lane (same addresses: broadcasts; no shuffle of the result)
         int first = 0x7fffffff;
-        for (int t = lane; t < q.n2; t += 32)
-            if (((volatile unsigned long long*)q.l2)[(int64_t)hi * q.n2 + t] != 0ull) {
-                first = t;
-                break;
-            }
-        for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-        int i = 0;
-        if (lane == 0) {
-            const unsigned long long x2 = ((volatile unsigned long long*)q.l2)[(int64_t)hi * q.n2 + first];
+        const unsigned long long* l2b = q.l2 + (int64_t)hi * q.n2;
+        if (q.n2 <= 32) {
+            const bool nz = lane < q.n2 && ((volatile const unsigned long long*)l2b)[lane] != 0ull;
+            first = __ffs(__ballot_sync(0xffffffffu, nz)) - 1;
+        } else {
+            for (int t = lane; t < q.n2; t += 32)
+                if (((volatile const unsigned long long*)l2b)[t] != 0ull) {
+                    first = t;
+                    break;
+                }
+            for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+        }
+        int i;
+        {
+            const unsigned long long x2 = ((volatile const unsigned long long*)l2b)[first];
             const int w1 = first * 64 + __ffsll((long long)x2) - 1;
             const unsigned long long x1 = ((volatile unsigned long long*)q.l1)[(int64_t)hi * q.n1 + w1];
             const int w0 = w1 * 64 + __ffsll((long long)x1) - 1;
@@ -656,7 +664,6 @@ __global__ void __launch_bounds__(kRsWinThreads) k_rs_select_win(const int* __re
                                   : ((volatile unsigned long long*)q.l0)[(int64_t)hi * q.n0 + w0];
             i = w0 * 64 + __ffsll((long long)x0) - 1;
         }
-        i = __shfl_sync(0xffffffffu, i, 0);
         // move the window with the front: when the selection runs into the last
         // quarter, or lies outside twice in a row (an isolated far selection is
         // served from global memory)
