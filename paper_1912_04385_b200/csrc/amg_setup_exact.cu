@@ -945,13 +945,14 @@ __device__ void rs2_move(unsigned char* wm, signed char* mark, int n, int owb, i
 template <int PASS>
 __global__ void __launch_bounds__(kRs2Threads) k_rs2_seq_win(const int* __restrict__ srp, const int* __restrict__ sci,
                                                              signed char* mark, const int* __restrict__ cand, int ncand,
-                                                             int n) {
+                                                             int n, const int* __restrict__ rec, int recB, int recW) {
     extern __shared__ unsigned char rs2_sm[];
     unsigned char* wm = rs2_sm;
     const int lane = threadIdx.x & 31, tid = threadIdx.x;
     __shared__ int cil[4096];
     __shared__ int ncil;
     __shared__ int cmd[3];
+    __shared__ int recs[kRsRecMax];
     int wb = max(0, (cand[0] - kRs2Win / 4) & ~63), wn = min(kRs2Win, n - wb);
     rs2_move(wm, mark, n, 0, 0, wb, tid);
     __syncthreads();
@@ -990,6 +991,7 @@ __global__ void __launch_bounds__(kRs2Threads) k_rs2_seq_win(const int* __restri
         else
             mark[x] = kC;
     };
+    int pw0 = 0, pw1 = 0, pw2 = 0, pw3 = 0;  // prefetched record words (pass 2)
     for (int t = 0; t < ncand; ++t) {
         const int i = __ldg(cand + t);
         if (i - wb > kRs2Win - kRs2Win / 4 && wb + kRs2Win < n) move_window(max(0, (i - kRs2Win / 4) & ~63));
@@ -999,6 +1001,70 @@ __global__ void __launch_bounds__(kRs2Threads) k_rs2_seq_win(const int* __restri
                 if (get(__ldg(sci + p)) == kC) has_c = true;
             has_c = __any_sync(0xffffffffu, has_c);
             if (!has_c && lane == 0) set_c(i);
+            __syncwarp();
+            continue;
+        }
+        if (PASS == 2 && rec) {
+            // two-hop record of the candidate (S_i and the S_j of its members; built by
+            // k_rs_records over S twice): the next candidate's record is requested
+            // before this one is replayed, so the replay sees no global latency
+            if (t == 0) {
+                const int* rp_ = rec + (int64_t)recW * i + lane;
+                pw0 = __ldg(rp_);
+                if (recW > 32) pw1 = __ldg(rp_ + 32);
+                if (recW > 64) pw2 = __ldg(rp_ + 64);
+                if (recW > 96) pw3 = __ldg(rp_ + 96);
+            }
+            __syncwarp();
+            recs[lane] = pw0;
+            if (recW > 32) recs[32 + lane] = pw1;
+            if (recW > 64) recs[64 + lane] = pw2;
+            if (recW > 96) recs[96 + lane] = pw3;
+            if (t + 1 < ncand) {
+                const int* rp_ = rec + (int64_t)recW * __ldg(cand + t + 1) + lane;
+                pw0 = __ldg(rp_);
+                if (recW > 32) pw1 = __ldg(rp_ + 32);
+                if (recW > 64) pw2 = __ldg(rp_ + 64);
+                if (recW > 96) pw3 = __ldg(rp_ + 96);
+            }
+            if (lane == 0) ncil = 0;
+            __syncwarp();
+            if (get(i) != kF) continue;
+            const int ns = ((volatile int*)recs)[0];
+            // one lane per member of S_i: the C members seed the list, the F members
+            // (their marks cannot change before their own turn) are replayed in order
+            const int myj = lane < ns ? ((volatile int*)recs)[1 + lane * recB] : -1;
+            const signed char mj = lane < ns ? get(myj) : kU;
+            if (mj == kC) {
+                const int pos = atomicAdd(&ncil, 1);
+                if (pos < 4096) cil[pos] = myj;
+            }
+            unsigned fmask = __ballot_sync(0xffffffffu, mj == kF);
+            __syncwarp();
+            while (fmask) {
+                const int p = __ffs(fmask) - 1;
+                fmask &= fmask - 1;
+                const int j = __shfl_sync(0xffffffffu, myj, p);
+                const int nci = min(((volatile int*)&ncil)[0], 4096);
+                const int nsj = ((volatile int*)recs)[2 + p * recB];
+                bool shared = false;
+                if (lane < nsj) {
+                    const int k = ((volatile int*)recs)[3 + p * recB + lane];
+                    for (int e = 0; e < nci; ++e)
+                        if (((volatile int*)cil)[e] == k) {
+                            shared = true;
+                            break;
+                        }
+                }
+                shared = __any_sync(0xffffffffu, shared);
+                if (!shared && lane == 0) {
+                    set_c(j);
+                    const int pos = ncil;
+                    if (pos < 4096) cil[pos] = j;
+                    ncil = pos + 1;
+                }
+                __syncwarp();
+            }
             __syncwarp();
             continue;
         }
@@ -1446,7 +1512,7 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
     DBuf<int> scnt(n), stcnt(n), srp(n + 1), strp(n + 1), stfill(n);
     MG_CUDA(cudaMemsetAsync(stcnt.p, 0, sizeof(int) * n, c.s));
     MG_CUDA(cudaMemsetAsync(stfill.p, 0, sizeof(int) * n, c.s));
-    Trace tr_s(&c, "amg strength");
+    auto tr_s = std::make_unique<Trace>(&c, "amg strength");
     k_strength_count<<<nblk(n), 256, 0, c.s>>>(a.rp, a.ci, a.v, n, theta, mrow.p, scnt.p, stcnt.p);
     const int ns = scan(c, s, scnt.p, srp.p, n);
     scan(c, s, stcnt.p, strp.p, n);
@@ -1456,6 +1522,7 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
     k_sort_rows<<<nblk(n), 256, 0, c.s>>>(strp.p, stci.p, nullptr, n);
     check_launch("strength");
 
+    tr_s.reset();
     // ---- first pass: bucket queue
     int lmax = 0;
     {
@@ -1564,10 +1631,11 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
         }
     }
     // ---- second pass
-    Trace tr2(&c, "amg rs passes 2+3");
+    auto tr2 = std::make_unique<Trace>(&c, "amg rs pass 2");
     DBuf<int> flag(n), fpos(n + 1), list(n);
     k_rs2_cand<<<nblk(n), 256, 0, c.s>>>(srp.p, sci.p, mark, n, flag.p);
     int ncand = scan(c, s, flag.p, fpos.p, n);
+    if (trace_on()) fprintf(stderr, "[mprec] rs pass 2: n=%d candidates %d\n", n, ncand);
     if (ncand) {
         k_compact<<<nblk(n), 256, 0, c.s>>>(flag.p, fpos.p, n, list.p);
         static const bool win2_on = [] {
@@ -1581,12 +1649,33 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
                 MG_CUDA(cudaFuncSetAttribute(k_rs2_seq_win<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRs2Win));
                 attr = true;
             }
-            k_rs2_seq_win<2><<<1, kRs2Threads, kRs2Win, c.s>>>(srp.p, sci.p, mark, list.p, ncand, n);
+            // S-S two-hop records (the first pass's builder with S in both hops)
+            DBuf<int> rec2;
+            int rB = 0, rW = 0;
+            {
+                int smax = 0;
+                DBuf<int> mx2(1);
+                MG_CUDA(cudaMemsetAsync(mx2.p, 0, sizeof(int), c.s));
+                k_max_int<<<std::min(nblk(n), 1024), 256, 0, c.s>>>(scnt.p, n, mx2.p);
+                MG_CUDA(cudaMemcpyAsync(&smax, mx2.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+                c.sync();
+                const int B = 2 + smax, RW = (1 + smax * B + 31) & ~31;
+                const char* e = getenv("MPREC_RS_RECORDS");
+                if (!(e && e[0] == '0') && RW <= kRsRecMax && smax <= 32) {
+                    rB = B;
+                    rW = RW;
+                    rec2.alloc((size_t)RW * n);
+                    k_rs_records<<<nblk(n), 256, 0, c.s>>>(srp.p, sci.p, srp.p, sci.p, n, B, RW, rec2.p);
+                }
+            }
+            k_rs2_seq_win<2><<<1, kRs2Threads, kRs2Win, c.s>>>(srp.p, sci.p, mark, list.p, ncand, n, rec2.p, rB, rW);
         } else {
             k_rs2_seq<<<1, 32, 0, c.s>>>(srp.p, sci.p, mark, list.p, ncand);
         }
         check_launch("rs second pass");
     }
+    tr2.reset();
+    auto tr2b = std::make_unique<Trace>(&c, "amg rs pass 3");
     // ---- third pass
     k_rs3_cand<<<nblk(n), 256, 0, c.s>>>(srp.p, sci.p, mark, n, flag.p);
     ncand = scan(c, s, flag.p, fpos.p, n);
@@ -1602,12 +1691,13 @@ static int rs_coarsen(Ctx& c, Scratch& s, const CsrView& a, double theta, DBuf<s
                 MG_CUDA(cudaFuncSetAttribute(k_rs2_seq_win<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRs2Win));
                 attr3 = true;
             }
-            k_rs2_seq_win<3><<<1, kRs2Threads, kRs2Win, c.s>>>(srp.p, sci.p, mark, list.p, ncand, n);
+            k_rs2_seq_win<3><<<1, kRs2Threads, kRs2Win, c.s>>>(srp.p, sci.p, mark, list.p, ncand, n, nullptr, 0, 0);
         } else {
             k_rs3_seq<<<1, 32, 0, c.s>>>(srp.p, sci.p, mark, list.p, ncand);
         }
         check_launch("rs third pass");
     }
+    tr2b.reset();
     // ---- coarse ids + direct interpolation
     Trace tr3(&c, "amg interpolation");
     DBuf<int> isc(n), cpos(n + 1), pcnt(n);
