@@ -40,6 +40,7 @@ VARIANTS = {
     "gs-warp": {"MPREC_GS_MODE": "warp"},
     "rs-nowindow": {"MPREC_RS_WINDOW": "0"},  # RS passes without their shared-memory windows: same results
     "rs-small-window": {"MPREC_RS_BUDGET_KB": "24"},  # 4k-point window: it moves, selections fall outside
+    "rs-norecords": {"MPREC_RS_RECORDS": "0"},  # CSR walk instead of the two-hop adjacency records
 }
 
 
@@ -70,6 +71,7 @@ def test_rs_window_does_not_change_results():
     dflt = _run({}, False)
     assert _run(VARIANTS["rs-nowindow"], False) == dflt
     assert _run(VARIANTS["rs-small-window"], False) == dflt
+    assert _run(VARIANTS["rs-norecords"], False) == dflt
 
 
 def test_fused_residual_restriction_bitwise():
