@@ -497,7 +497,7 @@ __device__ __forceinline__ void rw_insert(const RsWin& w, const Buckets& q, int 
 
 // Window move, all kRsWinThreads threads of the block (the helper warps sleep on a
 // named barrier between moves): write the old window back, then load the new one.
-constexpr int kRsWinThreads = 256;
+constexpr int kRsWinThreads = 1024;  // one selecting warp + 31 warps that only move the window
 __device__ __forceinline__ void rw_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRsWinThreads) : "memory"); }
 
 __device__ void rw_move(unsigned char* st, unsigned char* lm, unsigned long long* wl0, int w64, const Buckets& q,
