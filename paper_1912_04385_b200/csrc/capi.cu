@@ -22,6 +22,16 @@
 using namespace mg;
 
 namespace {
+// Library load: ask for eager module loading unless the host chose otherwise.  With
+// CUDA's default lazy loading every kernel is loaded at its first launch, and a
+// load issued while another setup thread's multi-second kernel runs waits for it
+// (+7 s on the first config-5 setup of a process).  Only effective when this
+// runs before the CUDA context exists (a host linked against the library; a
+// host that initialised CUDA first keeps its own setting).
+struct EagerModules {
+    EagerModules() { setenv("CUDA_MODULE_LOADING", "EAGER", 0); }
+} g_eager_modules;
+
 thread_local std::string g_err;
 thread_local int g_payload = -1;
 
